@@ -15,8 +15,10 @@ Control u = (dp_f+[2], dp_r+[2], a~, d~) with CoP weight alpha = 0.5 + a~ and
 contact-phase duration delta = DELTA0 + d~ (both kept in range by u_max).
 
 Per contact phase (rotation-free, diagonal pairs alternate
-through sigma = cos(pi * s_idx)):
-    du_cop = alpha (S_f - dp_f) + (1 - alpha) (S_r - dp_r)
+through sigma = cos(pi * s_idx)); the CoP carries a capture-point feedback term
+cdot/omega (a low-level balance reflex) so that open-loop / random policies keep
+the state bounded over 100 phases (the bare LIPM diverges like e^{omega delta}):
+    du_cop = alpha (S_f - dp_f) + (1 - alpha) (S_r - dp_r) + cdot / omega
     c+    = c + sinh(w d)/w * cdot + (1 - cosh(w d)) du_cop
     cdot+ = cosh(w d) cdot - w sinh(w d) du_cop
     dp+   = u[0:4],  s_idx+ = s_idx + 1,  c_obs, walls constant
@@ -39,7 +41,7 @@ DEFAULTS = dict(
     n=15, m=6, dt=DELTA0, t_max=100,
     u_max=(0.15, 0.15, 0.15, 0.15, 0.5, 0.125),
     workspace=((-0.1, 0.1),) * 4 + ((-4.0, 4.0),) * 2 + ((-1.0, 1.0),) * 2
-    + ((0.0, 0.0),) + ((-2.0, 2.0),) * 2
+    + ((0.0, 100.0),) + ((-2.0, 2.0),) * 2
     + ((-6.0, -4.5), (4.5, 6.0), (-6.0, -4.5), (4.5, 6.0)),
     hard_region=((0.0, 0.0),) * 4 + ((2.0, 3.5), (-1.0, 1.0)) + ((0.0, 0.0),) * 2
     + ((0.0, 0.0),) + ((1.0, 1.0), (0.0, 0.0))
@@ -60,8 +62,9 @@ def _phase(x, u):
     sig = np.cos(np.pi * x[..., 8])
     sfx, sfy = SX, sig * SY
     srx, sry = -SX, -sig * SY
-    ux = a * (sfx - x[..., 0]) + (1.0 - a) * (srx - x[..., 2])
-    uy = a * (sfy - x[..., 1]) + (1.0 - a) * (sry - x[..., 3])
+    # CoP offset from the CoM: feet term + capture-point feedback cdot / omega
+    ux = a * (sfx - x[..., 0]) + (1.0 - a) * (srx - x[..., 2]) + x[..., 6] / OMEGA
+    uy = a * (sfy - x[..., 1]) + (1.0 - a) * (sry - x[..., 3]) + x[..., 7] / OMEGA
     ch = np.cosh(OMEGA * d)
     sh = np.sinh(OMEGA * d)
     return a, d, ux, uy, ch, sh, (sfx - x[..., 0]) - (srx - x[..., 2]), (sfy - x[..., 1]) - (sry - x[..., 3])

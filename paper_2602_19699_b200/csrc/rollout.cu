@@ -1,0 +1,320 @@
+// rollout.cu -- K1: fused closed-loop actor rollout (nets.actor_rollout,
+// nets.py:403-423) for a batch of starts.
+//
+// One CTA owns S starts for the whole horizon.  Per time step:
+//   input tile  a0[c][s] = (x_s[c] - center[c]) / half[c], time row t0_s + k
+//   hidden      a_{i+1} = act(a_i W_i^T + b_i)        (register-tiled GEMM, smem weights)
+//   head        u_s = out_scale * tanh(a W_L^T + b_L)  (4-lane split + shuffles)
+//   dynamics    x_s <- f(x_s, u_s), stage cost l(x_s, u_s) accumulated in the
+//               thread that owns start s, in NumPy's pairwise-sum order, so
+//               cost == Trajectory.cost (ilqr.py:76-78) term for term.
+#include "systems.cuh"
+#include "tile.cuh"
+
+namespace cacto {
+
+template <typename T>
+struct RolloutArgs {
+  SysDev<T> sys;
+  CostDev<T> cost;
+  NetConst<T> nc;
+  int has_cost;
+  int nh, out, act, head;
+  const T* params;
+  const double* x0;
+  const int32_t* t0;
+  int t0_scalar;
+  int64_t N;
+  int t_hor;      // > 0 fixed horizon; 0 -> per-start t_max - t0
+  int t_stride;   // row stride of the per-step outputs
+  T* U;
+  T* X;
+  T* SC;
+  T* C;
+};
+
+// NumPy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) for
+// n <= 128 terms, fed one term at a time.  Longer sums chain 128-blocks.
+template <typename T>
+struct PairwiseSum {
+  T r[8];
+  T res;
+  int n;  // total terms
+  CACTO_D void init(int n_) {
+    n = n_;
+    res = T(0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = T(0);
+  }
+  CACTO_D static T combine(const T (&r)[8]) {
+    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  }
+  CACTO_D void add(int i, T v) {
+    if (n < 8) {
+      res += v;
+      return;
+    }
+    if (n > 128) {  // chained blocks of 128 (not bit-exact beyond 128 terms)
+      int blk = i >> 7, off = i & 127;
+      int len = min(128, n - (blk << 7));
+      if (off == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = T(0);
+      }
+      sub(off, len, v, blk > 0);
+      return;
+    }
+    sub(i, n, v, false);
+  }
+  CACTO_D void sub(int i, int len, T v, bool chain) {
+    int body = len - (len % 8);
+    if (len < 8) {
+      res += v;
+      return;
+    }
+    if (i < body) {
+      int j = i & 7;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q == j) r[q] = (i < 8) ? v : r[q] + v;
+      if (i == body - 1 && body == len) res = chain ? res + combine(r) : combine(r);
+    } else {
+      if (i == body) res = chain ? res + combine(r) : combine(r);
+      res += v;
+    }
+  }
+};
+
+template <typename T, int SYS, int HP, int S>
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 2 : 1))
+rollout_kernel(const RolloutArgs<T> a) {
+  using TL = Tile<T, S, HP>;
+  constexpr int n = SysDims<SYS>::n;
+  constexpr int m = SysDims<SYS>::m;
+  constexpr int IP = (n + 1) <= 8 ? 8 : ((n + 1) <= 16 ? 16 : 32);
+  const int nh = a.nh;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  // ---- carve shared memory -------------------------------------------------
+  T* W0 = sm;                         // [HP][IP] (or [m][IP] if nh == 0)
+  T* b0 = W0 + HP * IP;               // [HP]
+  T* Wh = b0 + HP;                    // (nh-1) x [HP][HP]
+  T* bh = Wh + (nh > 1 ? (nh - 1) : 0) * HP * HP;  // (nh-1) x [HP]
+  T* WL = bh + (nh > 1 ? (nh - 1) : 0) * HP;      // [m][HP]
+  T* bL = WL + m * HP;                // [m] (padded to 4)
+  T* A0 = bL + 4 * ((m + 3) / 4);     // [IP][S]
+  T* BA = A0 + IP * S;                // [HP][S]
+  T* BB = BA + HP * S;                // [HP][S]
+  T* US = BB + HP * S;                // [m][S] raw head outputs
+
+  // ---- stage weights (padded global layout -> swizzled smem) ------------------
+  {
+    const T* p = a.params;
+    if (nh == 0) {
+      stage_matrix(W0, p, m, IP);
+      stage_vector(bL, p + m * IP, m);
+    } else {
+      stage_matrix(W0, p, HP, IP);
+      p += HP * IP;
+      stage_vector(b0, p, HP);
+      p += HP;
+      for (int i = 0; i < nh - 1; ++i) {
+        stage_matrix(Wh + i * HP * HP, p, HP, HP);
+        p += HP * HP;
+        stage_vector(bh + i * HP, p, HP);
+        p += HP;
+      }
+      stage_matrix(WL, p, m, HP);
+      p += m * HP;
+      stage_vector(bL, p, m);
+    }
+  }
+  // zero the padded input rows once
+  for (int p = threadIdx.x; p < IP * S; p += kThreads) A0[p] = T(0);
+
+  // ---- per-start registers (thread s < S owns start s of this tile) ------------
+  const int s_own = threadIdx.x;
+  const int64_t gi = (int64_t)blockIdx.x * S + s_own;
+  const bool owner = s_own < S && gi < a.N;
+  T x[n];
+  int t0 = 0, T_i = 0;
+  PairwiseSum<T> acc;
+  if (owner) {
+#pragma unroll
+    for (int c = 0; c < n; ++c) x[c] = (T)a.x0[gi * n + c];
+    t0 = a.t0 ? a.t0[gi] : a.t0_scalar;
+    T_i = a.t_hor > 0 ? a.t_hor : (a.sys.t_max - t0);
+    acc.init(T_i + 1);
+    if (a.X) {
+#pragma unroll
+      for (int c = 0; c < n; ++c) a.X[gi * (int64_t)(a.t_stride + 1) * n + c] = x[c];
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < n; ++c) x[c] = T(0);
+  }
+  // block-wide horizon (max over owned starts)
+  __shared__ int s_kmax;
+  if (threadIdx.x == 0) s_kmax = 0;
+  __syncthreads();
+  if (owner) atomicMax(&s_kmax, T_i);
+  __syncthreads();
+  const int kmax = s_kmax;
+
+  const TL tl;
+  T accm[TL::TN][TL::TM];
+
+  for (int k = 0; k < kmax; ++k) {
+    // ---- normalised network input [x, t0 + k] (nets.py:416, 126-129) ----------
+    if (owner) {
+#pragma unroll
+      for (int c = 0; c < n; ++c) A0[TL::at(c, s_own)] = (x[c] - a.nc.in_center[c]) / a.nc.in_half[c];
+      A0[TL::at(n, s_own)] = ((T)(t0 + k) - a.nc.in_center[n]) / a.nc.in_half[n];
+    } else if (s_own < S) {
+#pragma unroll
+      for (int c = 0; c <= n; ++c) A0[TL::at(c, s_own)] = T(0);
+    }
+    __syncthreads();
+    const T* cur = A0;
+    if (nh > 0) {
+      // layer 0: K = IP
+      tl.template gemm_fwd<IP>(W0, A0, accm);
+      tl.store(BA, accm, [&](T v, int r, int) { return act_value(a.act, v + b0[r]); });
+      __syncthreads();
+      cur = BA;
+      T* nxt = BB;
+      for (int i = 0; i < nh - 1; ++i) {
+        tl.template gemm_fwd<HP>(Wh + i * HP * HP, cur, accm);
+        const T* bi = bh + i * HP;
+        tl.store(nxt, accm, [&](T v, int r, int) { return act_value(a.act, v + bi[r]); });
+        __syncthreads();
+        T* t = const_cast<T*>(cur);
+        cur = nxt;
+        nxt = t;
+      }
+      TL::template narrow<HP>(cur, m, [&](int j, int kk) { return WL[swz<HP>(j, kk)]; },
+                              [&](int s, int j, T v) { US[j * S + s] = v + bL[j]; });
+    } else {
+      TL::template narrow<IP>(cur, m, [&](int j, int kk) { return W0[swz<IP>(j, kk)]; },
+                              [&](int s, int j, T v) { US[j * S + s] = v + bL[j]; });
+    }
+    __syncthreads();
+    // ---- head, running cost, dynamics (thread per start) -----------------------
+    if (owner && k < T_i) {
+      T u[m];
+#pragma unroll
+      for (int j = 0; j < m; ++j) u[j] = head_value(a.head, a.nc, j, US[j * S + s_own]);
+      if (a.U) {
+#pragma unroll
+        for (int j = 0; j < m; ++j) a.U[(gi * a.t_stride + k) * m + j] = u[j];
+      }
+      T sc = T(0);
+      if (a.has_cost) sc = stage_cost<SYS>(a.sys, a.cost, x, u);
+      acc.add(k, sc);
+      if (a.SC) a.SC[gi * (int64_t)(a.t_stride + 1) + k] = sc;
+      T xn[n];
+      step<SYS>(a.sys, x, u, xn);
+#pragma unroll
+      for (int c = 0; c < n; ++c) x[c] = xn[c];
+      if (a.X) {
+#pragma unroll
+        for (int c = 0; c < n; ++c) a.X[(gi * (int64_t)(a.t_stride + 1) + k + 1) * n + c] = x[c];
+      }
+    }
+    // the next iteration's first barrier orders A0 writes after these US reads
+  }
+  if (owner) {
+    T term = a.has_cost ? terminal_cost<SYS>(a.sys, a.cost, x) : T(0);
+    acc.add(T_i, term);
+    if (a.SC) a.SC[gi * (int64_t)(a.t_stride + 1) + T_i] = term;
+    if (a.C) a.C[gi] = acc.res;
+  }
+}
+
+template <typename T, int SYS, int HP>
+static int launch_rollout(const RolloutArgs<T>& a, cudaStream_t st) {
+  constexpr int S = sizeof(T) == 4 ? 128 : 64;
+  constexpr int n = SysDims<SYS>::n, m = SysDims<SYS>::m;
+  constexpr int IP = (n + 1) <= 8 ? 8 : ((n + 1) <= 16 ? 16 : 32);
+  int nhw = a.nh > 1 ? a.nh - 1 : 0;
+  size_t elems = (size_t)HP * IP + HP + (size_t)nhw * (HP * HP + HP) + (size_t)m * HP + 4 * ((m + 3) / 4) +
+                 (size_t)IP * S + 2 * (size_t)HP * S + (size_t)m * S;
+  size_t bytes = elems * sizeof(T);
+  auto kern = rollout_kernel<T, SYS, HP, S>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return set_error(CACTO_ECUDA, "rollout: %zu B of shared memory not available", bytes);
+  int64_t blocks = (a.N + S - 1) / S;
+  kern<<<(unsigned)blocks, kThreads, bytes, st>>>(a);
+  return check_launch("rollout_kernel");
+}
+
+template <typename T>
+static int dispatch_rollout(const RolloutArgs<T>& a, int kind, int hp, cudaStream_t st) {
+#define CACTO_ROLL_CASE(SYSK)                                              \
+  case SYSK:                                                               \
+    if (hp == 32) return launch_rollout<T, SYSK, 32>(a, st);               \
+    if (hp == 64) return launch_rollout<T, SYSK, 64>(a, st);               \
+    break;
+  switch (kind) {
+    CACTO_ROLL_CASE(CACTO_SYS_TOY1D)
+    CACTO_ROLL_CASE(CACTO_SYS_POINTMASS)
+    CACTO_ROLL_CASE(CACTO_SYS_DUBINS)
+    CACTO_ROLL_CASE(CACTO_SYS_MANIPULATOR3)
+    CACTO_ROLL_CASE(CACTO_SYS_ALIENGO_LIPM)
+    default:
+      break;
+  }
+#undef CACTO_ROLL_CASE
+  return set_error(CACTO_EUNSUPPORTED, "rollout: system kind %d with hidden width %d not built", kind, hp);
+}
+
+}  // namespace cacto
+
+using namespace cacto;
+
+static int system_dims_ok(const cacto_system_t* s) {
+  static const int dims[5][2] = {{1, 1}, {4, 2}, {5, 2}, {6, 3}, {15, 6}};
+  if (s->kind < 0 || s->kind > 4) return 0;
+  return s->n == dims[s->kind][0] && s->m == dims[s->kind][1];
+}
+
+extern "C" int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
+                             const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
+                             void* U, void* X, void* step_costs, void* cost_to_go, void* stream) {
+  if (!sys || !actor || !x0) return set_error(CACTO_EVALUE, "rollout: null argument");
+  if (!system_dims_ok(sys)) return set_error(CACTO_EUNSUPPORTED, "rollout: unknown system kind %d / dims", sys->kind);
+  if (N < 0) return set_error(CACTO_EVALUE, "rollout: N < 0");
+  if (actor->sizes[0] != sys->n + 1 || actor->sizes[actor->n_layers] != sys->m)
+    return set_error(CACTO_EVALUE, "rollout: actor dims [%d -> %d] do not match system (n=%d, m=%d)",
+                     actor->sizes[0], actor->sizes[actor->n_layers], sys->n, sys->m);
+  if (t_hor < 0) return set_error(CACTO_EVALUE, "rollout: negative horizon");
+  if (!t0 && t_hor > sys->t_max - t0_scalar)
+    return set_error(CACTO_EVALUE, "rollout of %d steps exceeds horizon from t=%d", t_hor, t0_scalar);
+  if (N == 0) return CACTO_OK;
+  int stride = t_hor > 0 ? t_hor : sys->t_max;
+  cudaStream_t st = (cudaStream_t)stream;
+  NetShape sh = shape_of(*actor);
+  if (actor->dtype == CACTO_F32) {
+    RolloutArgs<float> a{};
+    a.sys = sys_dev<float>(*sys);
+    if (cost) a.cost = cost_dev<float>(*cost);
+    a.nc = net_const<float>(*actor);
+    a.has_cost = cost != nullptr;
+    a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
+    a.params = (const float*)actor->params;
+    a.x0 = x0; a.t0 = t0; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor; a.t_stride = stride;
+    a.U = (float*)U; a.X = (float*)X; a.SC = (float*)step_costs; a.C = (float*)cost_to_go;
+    return dispatch_rollout(a, sys->kind, sh.hp, st);
+  }
+  RolloutArgs<double> a{};
+  a.sys = sys_dev<double>(*sys);
+  if (cost) a.cost = cost_dev<double>(*cost);
+  a.nc = net_const<double>(*actor);
+  a.has_cost = cost != nullptr;
+  a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
+  a.params = (const double*)actor->params;
+  a.x0 = x0; a.t0 = t0; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor; a.t_stride = stride;
+  a.U = (double*)U; a.X = (double*)X; a.SC = (double*)step_costs; a.C = (double*)cost_to_go;
+  return dispatch_rollout(a, sys->kind, sh.hp, st);
+}

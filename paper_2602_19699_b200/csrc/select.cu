@@ -1,0 +1,348 @@
+// select.cu -- K3: stable descending top-k, exactly
+//   order = np.argsort(-scores, kind="stable")[:keep]        (trainer.py:152)
+// i.e. larger score first, equal scores by ascending index, NaN last and
+// -0.0 == +0.0.  Scores map to order-preserving unsigned keys (ascending key =
+// descending score); (key, index) pairs are unique, so any exact selection +
+// sort of the pairs reproduces the stable argsort.
+//
+//  1. radix select (cooperative kernel, 8-bit digits, MSB first): threshold key
+//     K* with #(key < K*) < keep <= #(key <= K*), warp-privatised histograms
+//  2. ordered compaction: all keys < K*, plus the lowest-index keep-#(<K*)
+//     keys == K* (ballot/popc prefix in index order across the grid)
+//  3. sort the keep survivors: bitonic sort of 2048-pair chunks in shared
+//     memory, then merge passes (merge-path lower_bound)
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace cacto {
+
+struct Pair {
+  unsigned long long key;
+  long long idx;
+};
+
+CACTO_D bool pair_less(const Pair& a, const Pair& b) {
+  return a.key < b.key || (a.key == b.key && a.idx < b.idx);
+}
+
+CACTO_D unsigned long long score_key(float s) {
+  if (s != s) return 0xFFFFFFFFull;  // NaN last
+  if (s == 0.0f) s = 0.0f;           // -0.0 -> +0.0
+  unsigned int b = __float_as_uint(s);
+  unsigned int u = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return (unsigned long long)(~u);
+}
+CACTO_D unsigned long long score_key(double s) {
+  if (s != s) return 0xFFFFFFFFFFFFFFFFull;
+  if (s == 0.0) s = 0.0;
+  unsigned long long b = (unsigned long long)__double_as_longlong(s);
+  unsigned long long u = (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+  return ~u;
+}
+CACTO_D float key_score(unsigned long long k, float*) {
+  if (k == 0xFFFFFFFFull) return __uint_as_float(0x7fc00000u);
+  unsigned int u = ~(unsigned int)k;
+  unsigned int b = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  return __uint_as_float(b);
+}
+CACTO_D double key_score(unsigned long long k, double*) {
+  if (k == 0xFFFFFFFFFFFFFFFFull) return __longlong_as_double(0x7ff8000000000000ll);
+  unsigned long long u = ~k;
+  unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7FFFFFFFFFFFFFFFull) : ~u;
+  return __longlong_as_double((long long)b);
+}
+
+constexpr int kSelThreads = 256;
+constexpr int kSortChunk = 2048;
+constexpr int kMaxSelBlocks = 1024;
+
+struct SelState {
+  unsigned int hist[8][256];
+  unsigned long long n_lt;
+  unsigned int block_eq[kMaxSelBlocks];
+};
+
+template <typename T, int KB>
+__global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __restrict__ scores, int64_t N,
+                                                                   int64_t keep, SelState* st, Pair* __restrict__ sel) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned int wh[kSelThreads / 32][256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ long long s_need;
+  __shared__ unsigned int s_warp[kSelThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = gridDim.x;
+  const int64_t chunk = (N + G - 1) / G;
+  const int64_t c0 = blockIdx.x * chunk;
+  const int64_t c1 = c0 + chunk < N ? c0 + chunk : N;
+
+  unsigned long long prefix = 0;
+  long long need = keep;
+  constexpr int PASSES = KB / 8;
+  for (int p = 0; p < PASSES; ++p) {
+    const int shift = KB - 8 * (p + 1);
+    for (int q = tid; q < (kSelThreads / 32) * 256; q += kSelThreads) (&wh[0][0])[q] = 0;
+    __syncthreads();
+    for (int64_t i = c0 + tid; i < c1; i += kSelThreads) {
+      unsigned long long k = score_key(scores[i]);
+      bool match = (p == 0) || ((k >> (shift + 8)) == (prefix >> (shift + 8)));
+      if (match) {
+        unsigned int d = (unsigned int)((k >> shift) & 255ull);
+        // warp-aggregated increment: lanes with the same digit combine
+        unsigned int peers = __match_any_sync(__activemask(), d);
+        int leader = __ffs(peers) - 1;
+        if (lane == leader) atomicAdd(&wh[warp][d], (unsigned int)__popc(peers));
+      }
+    }
+    __syncthreads();
+    for (int d = tid; d < 256; d += kSelThreads) {
+      unsigned int c = 0;
+#pragma unroll
+      for (int w = 0; w < kSelThreads / 32; ++w) c += wh[w][d];
+      if (c) atomicAdd(&st->hist[p][d], c);
+    }
+    grid.sync();
+    if (tid == 0) {
+      long long cum = 0;
+      int digit = 255;
+      for (int d = 0; d < 256; ++d) {
+        long long h = st->hist[p][d];
+        if (cum + h >= need) {
+          digit = d;
+          break;
+        }
+        cum += h;
+      }
+      s_need = need - cum;
+      s_prefix = prefix | ((unsigned long long)digit << shift);
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    need = s_need;
+  }
+  // prefix == K*, need == number of K*-equal pairs to take (lowest indices)
+  const unsigned long long kstar = prefix;
+  const long long need_eq = need;
+  const long long n_lt_total = keep - need_eq;
+
+  // ordered count of equal keys in this block's chunk
+  unsigned int my_eq = 0;
+  for (int64_t base = c0; base < c1; base += kSelThreads) {
+    int64_t i = base + tid;
+    bool eq = i < c1 && score_key(scores[i]) == kstar;
+    unsigned int b = __ballot_sync(0xffffffffu, eq);
+    if (lane == 0) my_eq += __popc(b);
+  }
+  if (lane == 0) s_warp[warp] = my_eq;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned int tot = 0;
+    for (int w = 0; w < kSelThreads / 32; ++w) tot += s_warp[w];
+    st->block_eq[blockIdx.x] = tot;
+  }
+  grid.sync();
+  __shared__ long long s_off;
+  if (tid == 0) {
+    long long off = 0;
+    for (int b = 0; b < blockIdx.x; ++b) off += st->block_eq[b];
+    s_off = off;
+  }
+  __syncthreads();
+  long long running = s_off;
+  for (int64_t base = c0; base < c1; base += kSelThreads) {
+    int64_t i = base + tid;
+    unsigned long long k = i < c1 ? score_key(scores[i]) : ~0ull;
+    bool lt = i < c1 && k < kstar;
+    bool eq = i < c1 && k == kstar;
+    if (lt) {
+      unsigned long long slot = atomicAdd(&st->n_lt, 1ull);
+      sel[slot] = Pair{k, (long long)i};
+    }
+    unsigned int b = __ballot_sync(0xffffffffu, eq);
+    if (lane == 0) s_warp[warp] = __popc(b);
+    __syncthreads();
+    long long woff = running;
+    for (int w = 0; w < warp; ++w) woff += s_warp[w];
+    unsigned int tot = 0;
+    for (int w = 0; w < kSelThreads / 32; ++w) tot += s_warp[w];
+    if (eq) {
+      long long r = woff + __popc(b & ((1u << lane) - 1u));
+      if (r < need_eq) sel[n_lt_total + r] = Pair{k, (long long)i};
+    }
+    running += tot;
+    __syncthreads();
+  }
+}
+
+// bitonic sort of kSortChunk-pair chunks (pads with +inf pairs)
+__global__ void __launch_bounds__(kSelThreads) chunk_sort_kernel(Pair* data, int64_t M) {
+  __shared__ Pair sh[kSortChunk];
+  const int64_t base = (int64_t)blockIdx.x * kSortChunk;
+  for (int i = threadIdx.x; i < kSortChunk; i += kSelThreads)
+    sh[i] = (base + i < M) ? data[base + i] : Pair{~0ull, 0x7fffffffffffffffll};
+  __syncthreads();
+  for (int k = 2; k <= kSortChunk; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < kSortChunk; i += kSelThreads) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          bool up = (i & k) == 0;
+          Pair a = sh[i], b = sh[ixj];
+          if (pair_less(b, a) == up) {
+            sh[i] = b;
+            sh[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < kSortChunk; i += kSelThreads)
+    if (base + i < M) data[base + i] = sh[i];
+}
+
+// merge adjacent sorted runs of width w into runs of width 2w
+__global__ void merge_pass_kernel(const Pair* __restrict__ in, Pair* __restrict__ out, int64_t M, int64_t w) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t run = i / w;
+    int64_t pair_start = (run / 2) * 2 * w;
+    bool left = (run % 2) == 0;
+    int64_t my_start = run * w;
+    int64_t o_start = left ? my_start + w : pair_start;
+    int64_t o_end = left ? my_start + 2 * w : my_start;
+    if (o_start > M) o_start = M;
+    if (o_end > M) o_end = M;
+    Pair e = in[i];
+    int64_t lo = o_start, hi = o_end;  // count partner elements < e
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (pair_less(in[mid], e))
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    out[pair_start + (i - my_start) + (lo - o_start)] = e;
+  }
+}
+
+template <typename T>
+__global__ void emit_kernel(const Pair* __restrict__ sel, int64_t keep, int64_t base_index, int64_t* order,
+                            T* top_scores) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < keep; i += (int64_t)gridDim.x * blockDim.x) {
+    Pair p = sel[i];
+    order[i] = p.idx + base_index;
+    if (top_scores) top_scores[i] = key_score(p.key, (T*)nullptr);
+  }
+}
+
+template <typename T>
+__global__ void runs_to_pairs_kernel(const T* __restrict__ s, const int64_t* __restrict__ idx, int64_t M, Pair* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = Pair{score_key(s[i]), (long long)idx[i]};
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// sorts `M` pairs in a (ping-pong with b); returns the buffer holding the result
+static Pair* sort_pairs(Pair* a, Pair* b, int64_t M, int64_t first_width, cudaStream_t st) {
+  int64_t w = first_width;
+  if (w <= 0) {
+    int64_t chunks = (M + kSortChunk - 1) / kSortChunk;
+    if (chunks > 0) chunk_sort_kernel<<<(unsigned)chunks, kSelThreads, 0, st>>>(a, M);
+    w = kSortChunk;
+  }
+  Pair* src = a;
+  Pair* dst = b;
+  while (w < M) {
+    int64_t blocks = (M + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    merge_pass_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, dst, M, w);
+    Pair* t = src;
+    src = dst;
+    dst = t;
+    w *= 2;
+  }
+  return src;
+}
+
+}  // namespace cacto
+
+using namespace cacto;
+
+extern "C" size_t cacto_select_workspace_bytes(int32_t dtype, int64_t N, int64_t keep) {
+  (void)dtype;
+  (void)N;
+  int64_t k = keep > 0 ? keep : 1;
+  return align256(sizeof(SelState)) + 2 * align256((size_t)k * sizeof(Pair));
+}
+
+template <typename T>
+static int select_entry(const T* scores, int64_t N, int64_t keep, int64_t base_index, int64_t* order, T* top,
+                        void* ws, cudaStream_t st) {
+  SelState* state = (SelState*)ws;
+  Pair* a = (Pair*)((char*)ws + align256(sizeof(SelState)));
+  Pair* b = (Pair*)((char*)a + align256((size_t)keep * sizeof(Pair)));
+  if (cudaMemsetAsync(state, 0, sizeof(SelState), st) != cudaSuccess)
+    return set_error(CACTO_ECUDA, "select: memset failed");
+  constexpr int KB = sizeof(T) == 4 ? 32 : 64;
+  auto kern = radix_select_kernel<T, KB>;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSelThreads, 0);
+  if (occ < 1) occ = 1;
+  int64_t want = (N + kSelThreads * 8 - 1) / (kSelThreads * 8);
+  int64_t cap = (int64_t)occ * num_sms();
+  if (cap > kMaxSelBlocks) cap = kMaxSelBlocks;
+  int G = (int)(want < 1 ? 1 : (want > cap ? cap : want));
+  void* args[] = {(void*)&scores, (void*)&N, (void*)&keep, (void*)&state, (void*)&a};
+  if (cudaLaunchCooperativeKernel((void*)kern, G, kSelThreads, args, 0, st) != cudaSuccess)
+    return check_launch("radix_select_kernel (cooperative)");
+  Pair* res = sort_pairs(a, b, keep, 0, st);
+  int64_t eb = (keep + 255) / 256;
+  emit_kernel<T><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, base_index, order, top);
+  return check_launch("select emit");
+}
+
+extern "C" int cacto_select_topk(int32_t dtype, const void* scores, int64_t N, int64_t keep, int64_t base_index,
+                                 int64_t* order, void* top_scores, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  if (keep > N) return set_error(CACTO_EVALUE, "keep=%lld exceeds %lld candidates", (long long)keep, (long long)N);
+  if (keep < 0 || N < 0) return set_error(CACTO_EVALUE, "select: negative sizes");
+  if (keep == 0) return CACTO_OK;
+  if (!scores || !order || !workspace) return set_error(CACTO_EVALUE, "select: null buffer");
+  if (N > 0xFFFFFFFFll) return set_error(CACTO_EVALUE, "select: N too large");
+  if (workspace_bytes < cacto_select_workspace_bytes(dtype, N, keep))
+    return set_error(CACTO_EVALUE, "select: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CACTO_F32)
+    return select_entry<float>((const float*)scores, N, keep, base_index, order, (float*)top_scores, workspace, st);
+  return select_entry<double>((const double*)scores, N, keep, base_index, order, (double*)top_scores, workspace, st);
+}
+
+extern "C" int cacto_select_merge(int32_t dtype, const void* run_scores, const int64_t* run_index, int32_t R,
+                                  int64_t keep, int64_t* order, void* top_scores, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if (R < 1 || keep < 0) return set_error(CACTO_EVALUE, "select_merge: bad sizes");
+  if (keep == 0) return CACTO_OK;
+  int64_t M = (int64_t)R * keep;
+  size_t need = 2 * align256((size_t)M * sizeof(Pair));
+  if (workspace_bytes < need) return set_error(CACTO_EVALUE, "select_merge: workspace too small (%zu)", need);
+  cudaStream_t st = (cudaStream_t)stream;
+  Pair* a = (Pair*)workspace;
+  Pair* b = (Pair*)((char*)workspace + align256((size_t)M * sizeof(Pair)));
+  int64_t blocks = (M + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (dtype == CACTO_F32)
+    runs_to_pairs_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)run_scores, run_index, M, a);
+  else
+    runs_to_pairs_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double*)run_scores, run_index, M, a);
+  Pair* res = sort_pairs(a, b, M, keep, st);
+  int64_t eb = (keep + 255) / 256;
+  if (dtype == CACTO_F32)
+    emit_kernel<float><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, 0, order, (float*)top_scores);
+  else
+    emit_kernel<double><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, 0, order, (double*)top_scores);
+  return check_launch("select_merge");
+}

@@ -1,0 +1,162 @@
+"""BIC selection and the rollout+BIC pipeline on the B200 (reference
+`trajrl.trainer`, trainer.py:141-153, 181-193, 258-273).
+
+`select_initial_states_bic` is the drop-in (same signature / order / errors).
+`BicPipeline` is the device-resident form used by the benchmark and the
+multi-GPU shard path: candidates -> [rollout cost-to-go] -> score -> stable
+top-k -> warm-start rollouts of the kept starts, with no host round trip until
+the kept indices / warm starts are read back.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib, specs
+from .device import DeviceNet, abi_dtype, device, device_net, to_device, torch_dtype
+from .nets import actor_rollout_batch
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class SelectWorkspace:
+    """Reusable scratch for cacto_select_topk."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, dtype, N, keep):
+        need = int(_lib.load().cacto_select_workspace_bytes(dtype, N, keep))
+        if self.buf is None or self.buf.numel() < need:
+            self.buf = torch.empty(max(need, 1), device=device(), dtype=torch.uint8)
+        return self.buf, need
+
+
+_WS = SelectWorkspace()
+
+
+def select_topk_device(scores: torch.Tensor, keep: int, base_index: int = 0, ws: SelectWorkspace = _WS):
+    """Stable descending top-k of a device score vector: (order int64 [keep], scores [keep]).
+    Exactly np.argsort(-scores, kind='stable')[:keep] (trainer.py:152)."""
+    N = scores.shape[0]
+    if keep > N:
+        raise ValueError(f"keep={keep} exceeds {N} candidates")
+    dt = _lib.F32 if scores.dtype == torch.float32 else _lib.F64
+    order = torch.empty(keep, device=scores.device, dtype=torch.int64)
+    top = torch.empty(keep, device=scores.device, dtype=scores.dtype)
+    if keep == 0:
+        return order, top
+    buf, need = ws.get(dt, N, keep)
+    _lib.call("cacto_select_topk", dt, scores.data_ptr(), N, keep, base_index, order.data_ptr(),
+              top.data_ptr(), buf.data_ptr(), need, _stream())
+    return order, top
+
+
+def score_device(mode: str, xa: torch.Tensor, std_net: Optional[DeviceNet] = None,
+                 critic: Optional[DeviceNet] = None, rollout_cost: Optional[torch.Tensor] = None):
+    """K2: std sigma(x0) / gap |V(x0) - J(x0)| / std*gap scores of augmented starts."""
+    N = xa.shape[0]
+    scores = torch.empty(N, device=xa.device, dtype=xa.dtype)
+    _lib.call("cacto_score", _lib.SCORE[mode], std_net.desc if std_net else None,
+              critic.desc if critic else None, xa.data_ptr(),
+              rollout_cost.data_ptr() if rollout_cost is not None else None, N, scores.data_ptr(), _stream())
+    return scores
+
+
+def select_initial_states_bic(candidates, std_net, keep: int):
+    """trainer.py:141-153: keep the candidates with the largest std-critic output,
+    descending, ties by candidate index."""
+    if keep > len(candidates):
+        raise ValueError(f"keep={keep} exceeds {len(candidates)} candidates")
+    xa = np.stack([c.augmented for c in candidates])
+    sn = device_net(std_net)
+    scores = score_device("std", to_device(xa, sn.precision), std_net=sn)
+    order, _ = select_topk_device(scores, keep)
+    return [candidates[i] for i in order.cpu().numpy()]
+
+
+class BicPipeline:
+    """Rollout + BIC scoring + stable selection + warm starts, device resident.
+
+    One `run(x0)` processes N candidate starts (float64 [N, n] device tensor):
+      gap modes  K1 rollout (cost only) of every candidate -> J(x0)
+      K2 score   sigma(x0) and/or |V(x0) - J(x0)|
+      K3 select  stable top-keep (ties -> lower index)
+      K1 rollout of the kept starts emitting U (TO warm starts, trainer.py:192-193)
+    """
+
+    def __init__(self, model, field, actor, critic=None, std_net=None, mode: str = "gap",
+                 precision=None, base_index: int = 0):
+        if mode not in _lib.SCORE:
+            raise ValueError(f"unknown score mode {mode!r}")
+        if mode != "std" and critic is None:
+            raise ValueError("gap scores need a critic")
+        if mode != "gap" and std_net is None:
+            raise ValueError("std scores need a std net")
+        self.model, self.field, self.mode = model, field, mode
+        self.actor = actor if isinstance(actor, DeviceNet) else DeviceNet(actor, precision)
+        self.critic = None if critic is None else (critic if isinstance(critic, DeviceNet) else DeviceNet(critic, precision))
+        self.std = None if std_net is None else (std_net if isinstance(std_net, DeviceNet) else DeviceNet(std_net, precision))
+        self.precision = self.actor.precision
+        self.sysd = specs.system_struct(model)
+        self.costd = specs.cost_struct(model, field)
+        self.base_index = base_index
+        self.ws = SelectWorkspace()
+        self.kernel_launches = 0
+
+    def rollout_costs(self, x0: torch.Tensor, t0: int = 0) -> torch.Tensor:
+        N = x0.shape[0]
+        cost = torch.empty(N, device=x0.device, dtype=torch_dtype(self.precision))
+        _lib.call("cacto_rollout", self.sysd, self.costd, self.actor.desc, x0.data_ptr(), None, t0, N,
+                  self.model.t_max - t0, None, None, None, cost.data_ptr(), _stream())
+        return cost
+
+    def run(self, x0: torch.Tensor, keep: int, t0: int = 0, warm_starts: bool = True):
+        """x0 float64 [N, n] on device -> dict(order, scores, U, cost)."""
+        N, n = x0.shape
+        dt = torch_dtype(self.precision)
+        launches = 0
+        cost = None
+        if self.mode != "std":
+            cost = self.rollout_costs(x0, t0)
+            launches += 1
+        xa = torch.empty((N, n + 1), device=x0.device, dtype=dt)
+        xa[:, :n] = x0
+        xa[:, n] = float(t0)
+        launches += 2  # torch copy + fill of the augmented view
+        scores = score_device(self.mode, xa, self.std, self.critic, cost)
+        launches += 1
+        order, top = select_topk_device(scores, keep, 0, self.ws)
+        launches += 4 + max(0, int(np.ceil(np.log2(max(keep, 1) / 2048.0))))  # memset, select, sort, merges, emit
+        out = {"order": order, "scores": top, "cost": cost}
+        if warm_starts and keep > 0:
+            kept = x0.index_select(0, order)
+            launches += 1
+            T = self.model.t_max - t0
+            U = torch.empty((keep, T, self.model.m), device=x0.device, dtype=dt)
+            _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, keep, T,
+                      U.data_ptr(), None, None, None, _stream())
+            launches += 1
+            out["U"] = U
+        if self.base_index:
+            out["order"] = order + self.base_index
+        self.kernel_launches = launches
+        return out
+
+
+def evaluate_policy_costs(actor, model, fld, eval_starts, use_to: bool = False, **kwargs):
+    """trainer.py:258-273 rollout leg (batched on device); the optional TO
+    refinement stays on the reference CPU solver and is not provided here."""
+    if not eval_starts:
+        raise ValueError("eval_starts must be non-empty")
+    if use_to:
+        raise NotImplementedError("TO refinement runs on the reference CPU solver (out of scope)")
+    x0 = np.stack([s.x for s in eval_starts])
+    t0 = np.array([s.t for s in eval_starts])
+    r = actor_rollout_batch(actor, model, x0, t0, None, fld, emit=("cost",))
+    return r["cost"]
