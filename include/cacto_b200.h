@@ -104,7 +104,9 @@ typedef struct cacto_cost {
 
 /* Replay rows (reference `SampleBatch` columns, buffer.py:39-55 / ring buffer.py:97-101).
  * If `idx` is non-NULL, sample b reads row idx[b] of the columns (fused gather,
- * buffer.py:136-138); otherwise rows 0..rows-1. */
+ * buffer.py:136-138); otherwise rows 0..rows-1.  If `cycle` is non-NULL the
+ * index list is idx + (*cycle) * idx_stride, read on device at kernel run time,
+ * so one captured CUDA graph replays successive minibatches (trainer.py:211-233). */
 typedef struct cacto_batch {
   int32_t dtype;
   int32_t n, m, t_max;
@@ -116,6 +118,8 @@ typedef struct cacto_batch {
   const void* v_bar;       /* [*]      */
   const void* v_bar_x;     /* [*, n]   */
   const void* xa_plus_k;   /* [*, n+1] */
+  const int64_t* cycle;    /* optional device counter selecting the index list      */
+  int64_t idx_stride;      /* elements between successive index lists              */
 } cacto_batch_t;
 
 /* -- library ---------------------------------------------------------------- */
@@ -162,7 +166,10 @@ int cacto_select_topk(int32_t dtype, const void* scores, int64_t N, int64_t keep
                       int64_t* order, void* top_scores, void* workspace, size_t workspace_bytes,
                       void* stream);
 /* merge R sorted (score, index) runs of length `keep` each (allgathered shard
- * winners) into the global top-`keep` with the same order semantics. */
+ * winners) into the global top-`keep` with the same order semantics.  The
+ * index may be the global candidate index or, for contiguous shards in rank
+ * order, the position in the concatenated runs (same tie order); index < 0
+ * marks a padding row, which sorts after everything (including NaN). */
 int cacto_select_merge(int32_t dtype, const void* run_scores, const int64_t* run_index, int32_t R,
                        int64_t keep, int64_t* order, void* top_scores, void* workspace,
                        size_t workspace_bytes, void* stream);
@@ -211,6 +218,17 @@ int cacto_polyak(int32_t dtype, void* target, const void* online, int64_t P, dou
 int cacto_reduce_adam(int32_t dtype, const void* workspace, int32_t n_partials, int64_t P, void* params,
                       void* m, void* v, int64_t step, double lr, double beta1, double beta2, double eps,
                       void* target, double tau, void* grad_out, void* loss_out, void* stream);
+
+/* graph-replayable form: the step is *step_base + *counter (both device), the bias
+ * corrections come from device tables bc1[t] = 1 - beta1^t, bc2[t] = 1 - beta2^t
+ * (computed on the host like the reference), and the loss of this update is
+ * written to loss_base[*counter] (trainer.py:226). */
+int cacto_reduce_adam_graph(int32_t dtype, const void* workspace, int32_t n_partials, int64_t P, void* params,
+                            void* m, void* v, const int64_t* counter, const int64_t* step_base, const double* bc1,
+                            const double* bc2, double lr, double beta1, double beta2, double eps, void* target,
+                            double tau, void* loss_base, void* stream);
+/* ++(*counter) on device (closes one captured update cycle) */
+int cacto_counter_tick(int64_t* counter, void* stream);
 
 /* -- (a7) device PCG64 replay of Generator.uniform starts (envs/__init__.py:119-121)
  * x[i, j] = lo[j] + (hi[j]-lo[j]) * uniform draw (first_row + i)*n + j of the stream

@@ -56,7 +56,8 @@ class CactoBatch(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int32), ("n", ctypes.c_int32), ("m", ctypes.c_int32),
                 ("t_max", ctypes.c_int32), ("rows", ctypes.c_int64), ("denom", ctypes.c_int64),
                 ("idx", ctypes.c_void_p), ("xa", ctypes.c_void_p), ("u", ctypes.c_void_p),
-                ("v_bar", ctypes.c_void_p), ("v_bar_x", ctypes.c_void_p), ("xa_plus_k", ctypes.c_void_p)]
+                ("v_bar", ctypes.c_void_p), ("v_bar_x", ctypes.c_void_p), ("xa_plus_k", ctypes.c_void_p),
+                ("cycle", ctypes.c_void_p), ("idx_stride", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p
@@ -96,6 +97,9 @@ SIGNATURES = {
     "cacto_polyak": (ctypes.c_int, [_I32, _P, _P, _I64, _D, _P]),
     "cacto_reduce_adam": (ctypes.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _I64, _D, _D, _D, _D, _P, _D,
                                          _P, _P, _P]),
+    "cacto_reduce_adam_graph": (ctypes.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D,
+                                                _D, _P, _D, _P, _P]),
+    "cacto_counter_tick": (ctypes.c_int, [_P, _P]),
     "cacto_sample_states": (ctypes.c_int, [_U64, _U64, _U64, _U64, _I64, _I64, _I32, _P, _P, _P, _P]),
     "cacto_fma_peak": (ctypes.c_int, [_I32, _I32, _I32, _P, _P]),
 }

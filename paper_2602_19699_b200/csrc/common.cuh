@@ -58,6 +58,13 @@ CACTO_D T act_value(int act, T z) {
   if (act == CACTO_ACT_ELU) return z > T(0) ? z : m_expm1(z);
   return m_tanh(z);
 }
+// forward-pass activation: fp32 ELU uses the SFU exponential (__expf(z) - 1,
+// abs. error ~1e-7, inside the fp32 tolerance); fp64 keeps expm1 exactly
+CACTO_D float act_fast(int act, float z) {
+  if (act == CACTO_ACT_ELU) return z > 0.0f ? z : __expf(z) - 1.0f;
+  return tanhf(z);
+}
+CACTO_D double act_fast(int act, double z) { return act_value(act, z); }
 template <typename T>
 CACTO_D T act_d1(int act, T z) {
   if (act == CACTO_ACT_ELU) return z > T(0) ? T(1) : m_exp(z);
@@ -88,6 +95,43 @@ CACTO_D void st4(float* p, const V4<float>& v) {
 CACTO_D void st4(double* p, const V4<double>& v) {
   *reinterpret_cast<double2*>(p) = make_double2(v.v[0], v.v[1]);
   *reinterpret_cast<double2*>(p + 2) = make_double2(v.v[2], v.v[3]);
+}
+
+// ---- explicit shared-memory access (32-bit shared-window addresses) ---------
+// The tile loops address shared memory through 32-bit offsets so that every
+// access is an LDS/STS even when pointers pass through helper structs.
+CACTO_D uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+CACTO_D V4<float> lds4(uint32_t a, float*) {
+  V4<float> r;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+               : "r"(a));
+  return r;
+}
+CACTO_D V4<double> lds4(uint32_t a, double*) {
+  V4<double> r;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "r"(a));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[2]), "=d"(r.v[3]) : "r"(a + 16));
+  return r;
+}
+CACTO_D float lds1(uint32_t a, float*) {
+  float r;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
+  return r;
+}
+CACTO_D double lds1(uint32_t a, double*) {
+  double r;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(a));
+  return r;
+}
+CACTO_D void sts4(uint32_t a, const V4<float>& v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.v[0]), "f"(v.v[1]), "f"(v.v[2]),
+               "f"(v.v[3])
+               : "memory");
+}
+CACTO_D void sts4(uint32_t a, const V4<double>& v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.v[0]), "d"(v.v[1]) : "memory");
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a + 16), "d"(v.v[2]), "d"(v.v[3]) : "memory");
 }
 
 // ---- padded parameter layout (see include/cacto_b200.h) --------------------
@@ -183,6 +227,10 @@ CACTO_D T head_chain(int head, const NetConst<T>& c, int j, T o) {
   if (head == CACTO_HEAD_STD) return sigmoid(o);
   return T(1);
 }
+
+// set the dynamic shared-memory opt-in of a kernel once (idempotent, so no
+// runtime attribute call happens inside a CUDA-graph capture after warm-up)
+bool ensure_smem(const void* kernel, size_t bytes);
 
 inline int num_sms() {
   static int n = 0;

@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kThreads) mlp_forward_kernel(const FwdArgs<T> 
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  NetSm<T, HP, IP> net;
+  NetSmem<T, HP, IP, TL::KS> net;
   T* p = net.carve(sm, a.nh, a.in, a.out);
   T* A0 = p;
   T* P0 = A0 + IP * S;
@@ -37,11 +37,11 @@ __global__ void __launch_bounds__(kThreads) mlp_forward_kernel(const FwdArgs<T> 
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t base = t * S;
     __syncthreads();
-    load_input_tile<T, S>(A0, IP, a.in, a.nc, [&](int s) { return base + s < a.B ? base + s : (int64_t)-1; },
+    load_input_tile<TL>(A0, IP, a.in, a.nc, [&](int s) { return base + s < a.B ? base + s : (int64_t)-1; },
                           [&](int64_t r, int c) { return a.xa[r * a.in + c]; });
     __syncthreads();
-    const T* last = forward_hidden<T, S, HP, IP>(tl, net, a.act, A0, P0, P1, nullptr);
-    forward_output<T, S, HP, IP>(net, last, [&](int s, int j, T o) {
+    const T* last = forward_hidden(tl, net, a.act, A0, P0, P1, (T*)nullptr);
+    forward_output<TL>(net, last, [&](int s, int j, T o) {
       if (base + s < a.B) a.out_y[(base + s) * a.out + j] = head_value(a.head, a.nc, j, o);
     });
   }
@@ -53,32 +53,30 @@ __global__ void __launch_bounds__(kThreads) mlp_jacobian_kernel(const FwdArgs<T>
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  NetSm<T, HP, IP> net;
+  NetSmem<T, HP, IP, TL::KS> net;
   T* p = net.carve(sm, a.nh, a.in, a.out);
   T* A0 = p;
   T* P0 = A0 + IP * S;
   T* P1 = P0 + HP * S;
   T* Zb = P1 + HP * S;  // nh x [HP][S]
   T* OUT = Zb + (size_t)(a.nh > 0 ? a.nh : 1) * HP * S;  // [out][S] raw outputs
-  T* Z[CACTO_MAX_LAYERS];
-  for (int i = 0; i < a.nh; ++i) Z[i] = Zb + (size_t)i * HP * S;
   net.stage(a.params);
   const TL tl;
   const int64_t ntiles = (a.B + S - 1) / S;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t base = t * S;
     __syncthreads();
-    load_input_tile<T, S>(A0, IP, a.in, a.nc, [&](int s) { return base + s < a.B ? base + s : (int64_t)-1; },
+    load_input_tile<TL>(A0, IP, a.in, a.nc, [&](int s) { return base + s < a.B ? base + s : (int64_t)-1; },
                           [&](int64_t r, int c) { return a.xa[r * a.in + c]; });
     __syncthreads();
-    const T* last = forward_hidden<T, S, HP, IP>(tl, net, a.act, A0, P0, P1, Z);
-    forward_output<T, S, HP, IP>(net, last, [&](int s, int j, T o) {
+    const T* last = forward_hidden(tl, net, a.act, A0, P0, P1, Zb);
+    forward_output<TL>(net, last, [&](int s, int j, T o) {
       OUT[j * S + s] = o;
       if (base + s < a.B) a.out_y[(base + s) * a.out + j] = head_value(a.head, a.nc, j, o);
     });
     __syncthreads();
     for (int j = 0; j < a.out; ++j) {
-      input_grad_sweep<T, S, HP, IP>(tl, net, a.act, j, Z, nullptr, P0, P1, [&](int s, int c, T v) {
+      input_grad_sweep(tl, net, a.act, j, Zb, (T*)nullptr, P0, P1, [&](int s, int c, T v) {
         if (base + s < a.B) {
           T chain = head_chain(a.head, a.nc, j, OUT[j * S + s]);
           a.out_jac[((base + s) * a.out + j) * a.in + c] = v * chain / a.nc.in_half[c];
@@ -110,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreArgs<T> a) {
   T* sm = reinterpret_cast<T*>(smem_raw);
   const bool need_std = a.mode != CACTO_SCORE_GAP;
   const bool need_crit = a.mode != CACTO_SCORE_STD;
-  NetSm<T, HP, IP> nstd, ncrit;
+  NetSmem<T, HP, IP, TL::KS> nstd, ncrit;
   T* p = sm;
   if (need_std) p = nstd.carve(p, a.nh_std, a.in, 1);
   if (need_crit) p = ncrit.carve(p, a.nh_crit, a.in, 1);
@@ -126,12 +124,12 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreArgs<T> a) {
     const int64_t base = t * S;
     __syncthreads();
     if (need_std) {
-      load_input_tile<T, S>(A0, IP, a.in, a.nc_std,
+      load_input_tile<TL>(A0, IP, a.in, a.nc_std,
                             [&](int s) { return base + s < a.N ? base + s : (int64_t)-1; },
                             [&](int64_t r, int c) { return a.xa[r * a.in + c]; });
       __syncthreads();
-      const T* last = forward_hidden<T, S, HP, IP>(tl, nstd, a.act_std, A0, P0, P1, nullptr);
-      forward_output<T, S, HP, IP>(nstd, last, [&](int s, int, T o) {
+      const T* last = forward_hidden(tl, nstd, a.act_std, A0, P0, P1, (T*)nullptr);
+      forward_output<TL>(nstd, last, [&](int s, int, T o) {
         T sig = head_value(a.head_std, a.nc_std, 0, o);
         SIG[s] = sig;
         if (a.mode == CACTO_SCORE_STD && base + s < a.N) a.scores[base + s] = sig;
@@ -139,12 +137,12 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreArgs<T> a) {
       __syncthreads();
     }
     if (need_crit) {
-      load_input_tile<T, S>(A0, IP, a.in, a.nc_crit,
+      load_input_tile<TL>(A0, IP, a.in, a.nc_crit,
                             [&](int s) { return base + s < a.N ? base + s : (int64_t)-1; },
                             [&](int64_t r, int c) { return a.xa[r * a.in + c]; });
       __syncthreads();
-      const T* last = forward_hidden<T, S, HP, IP>(tl, ncrit, a.act_crit, A0, P0, P1, nullptr);
-      forward_output<T, S, HP, IP>(ncrit, last, [&](int s, int, T v) {
+      const T* last = forward_hidden(tl, ncrit, a.act_crit, A0, P0, P1, (T*)nullptr);
+      forward_output<TL>(ncrit, last, [&](int s, int, T v) {
         if (base + s < a.N) {
           T gap = fabs(v - a.rollout_cost[base + s]);
           a.scores[base + s] = a.mode == CACTO_SCORE_GAP ? gap : SIG[s] * gap;
@@ -158,7 +156,7 @@ template <typename T, int HP, int IP, typename K>
 static int launch_tiles(K kern, size_t smem_elems, int64_t rows, cudaStream_t st, const char* name,
                         const void* args_ptr) {
   size_t bytes = smem_elems * sizeof(T);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_ECUDA, "%s: %zu B of shared memory not available", name, bytes);
   int64_t tiles = (rows + fwd_S<T>() - 1) / fwd_S<T>();
   int64_t grid = tiles < 4 * num_sms() ? tiles : 4 * num_sms();
@@ -170,7 +168,7 @@ static int launch_tiles(K kern, size_t smem_elems, int64_t rows, cudaStream_t st
 template <typename T, int HP, int IP>
 static int run_forward(const FwdArgs<T>& a, bool jac, cudaStream_t st) {
   constexpr int S = fwd_S<T>();
-  size_t net_el = NetSm<T, HP, IP>::elems(a.nh, a.out);
+  size_t net_el = net_elems<T, HP, IP>(a.nh, a.out);
   size_t el = net_el + (size_t)IP * S + 2 * (size_t)HP * S;
   if (jac) el += (size_t)(a.nh > 0 ? a.nh : 1) * HP * S + (size_t)a.out * S;
   int grid;
@@ -192,8 +190,8 @@ template <typename T, int HP, int IP>
 static int run_score(const ScoreArgs<T>& a, cudaStream_t st) {
   constexpr int S = fwd_S<T>();
   size_t el = (size_t)IP * S + 2 * (size_t)HP * S + S;
-  if (a.mode != CACTO_SCORE_GAP) el += NetSm<T, HP, IP>::elems(a.nh_std, 1);
-  if (a.mode != CACTO_SCORE_STD) el += NetSm<T, HP, IP>::elems(a.nh_crit, 1);
+  if (a.mode != CACTO_SCORE_GAP) el += net_elems<T, HP, IP>(a.nh_std, 1);
+  if (a.mode != CACTO_SCORE_STD) el += net_elems<T, HP, IP>(a.nh_crit, 1);
   auto kern = score_kernel<T, HP, IP>;
   int grid = launch_tiles<T, HP, IP>(kern, el, a.N, st, "score", &a);
   if (grid < 0) return grid;
@@ -319,6 +317,8 @@ struct RowsArgs {
   int nh, in, act, head, which;
   const T* params;
   const int64_t* idx;
+  const int64_t* cycle;
+  int64_t stride;
   const T* x;      // xa or xa_plus_k column
   const T* v_bar;
   int64_t rows;
@@ -331,29 +331,30 @@ __global__ void __launch_bounds__(kThreads) rows_forward_kernel(const RowsArgs<T
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  NetSm<T, HP, IP> net;
+  NetSmem<T, HP, IP, TL::KS> net;
   T* p = net.carve(sm, a.nh, a.in, 1);
   T* A0 = p;
   T* P0 = A0 + IP * S;
   T* P1 = P0 + HP * S;
   net.stage(a.params);
   const TL tl;
+  const int64_t* idx = (a.idx && a.cycle) ? a.idx + (*a.cycle) * a.stride : a.idx;
   const int64_t ntiles = (a.rows + S - 1) / S;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t base = t * S;
     __syncthreads();
-    load_input_tile<T, S>(A0, IP, a.in, a.nc,
-                          [&](int s) { return base + s < a.rows ? (a.idx ? a.idx[base + s] : base + s) : (int64_t)-1; },
+    load_input_tile<TL>(A0, IP, a.in, a.nc,
+                          [&](int s) { return base + s < a.rows ? (idx ? idx[base + s] : base + s) : (int64_t)-1; },
                           [&](int64_t r, int c) { return a.x[r * a.in + c]; });
     __syncthreads();
-    const T* last = forward_hidden<T, S, HP, IP>(tl, net, a.act, A0, P0, P1, nullptr);
-    forward_output<T, S, HP, IP>(net, last, [&](int s, int, T o) {
+    const T* last = forward_hidden(tl, net, a.act, A0, P0, P1, (T*)nullptr);
+    forward_output<TL>(net, last, [&](int s, int, T o) {
       int64_t b = base + s;
       if (b >= a.rows) return;
       if (a.which == 1) {
         a.out[b] = head_value(a.head, a.nc, 0, o);
       } else {
-        int64_t r = a.idx ? a.idx[b] : b;
+        int64_t r = idx ? idx[b] : b;
         a.out[b] = a.v_bar[r] - head_value(a.head, a.nc, 0, o);
       }
     });
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(kThreads) rows_forward_kernel(const RowsArgs<T
 template <typename T, int HP, int IP>
 static int run_rows(const RowsArgs<T>& a, cudaStream_t st) {
   constexpr int S = fwd_S<T>();
-  size_t el = NetSm<T, HP, IP>::elems(a.nh, 1) + (size_t)IP * S + 2 * (size_t)HP * S;
+  size_t el = net_elems<T, HP, IP>(a.nh, 1) + (size_t)IP * S + 2 * (size_t)HP * S;
   auto kern = rows_forward_kernel<T, HP, IP>;
   int grid = launch_tiles<T, HP, IP>(kern, el, a.rows, st, "rows_forward", &a);
   if (grid < 0) return grid;
@@ -379,6 +380,8 @@ static int rows_entry(const cacto_mlp_t* m, const cacto_batch_t* b, int which, v
   a.nh = sh.nh; a.in = sh.in; a.act = sh.act; a.head = sh.head; a.which = which;
   a.params = (const T*)m->params;
   a.idx = b->idx;
+  a.cycle = b->cycle;
+  a.stride = b->idx_stride;
   a.x = (const T*)(which == 1 ? b->xa_plus_k : b->xa);
   a.v_bar = (const T*)b->v_bar;
   a.rows = b->rows;

@@ -19,7 +19,9 @@ struct Cols {
 };
 
 template <typename T>
-__global__ void gather_kernel(Cols<T> c, const int64_t* __restrict__ idx, int64_t B) {
+__global__ void gather_kernel(Cols<T> c, const int64_t* __restrict__ idx, const int64_t* cycle, int64_t stride,
+                              int64_t B) {
+  if (cycle) idx += (*cycle) * stride;
   const int W = c.width[0] + c.width[1] + c.width[2] + c.width[3] + c.width[4];
   const int64_t total = B * W;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -143,12 +145,14 @@ extern "C" int cacto_gather(const cacto_batch_t* ring, void* xa, void* u, void* 
     Cols<float> c = batch_cols<float>(ring);
     c.dst[0] = (float*)xa; c.dst[1] = (float*)u; c.dst[2] = (float*)v_bar; c.dst[3] = (float*)v_bar_x;
     c.dst[4] = (float*)xa_plus_k;
-    gather_kernel<float><<<grid_for(ring->rows * W), 256, 0, st>>>(c, ring->idx, ring->rows);
+    gather_kernel<float><<<grid_for(ring->rows * W), 256, 0, st>>>(c, ring->idx, ring->cycle, ring->idx_stride,
+                                                                    ring->rows);
   } else {
     Cols<double> c = batch_cols<double>(ring);
     c.dst[0] = (double*)xa; c.dst[1] = (double*)u; c.dst[2] = (double*)v_bar; c.dst[3] = (double*)v_bar_x;
     c.dst[4] = (double*)xa_plus_k;
-    gather_kernel<double><<<grid_for(ring->rows * W), 256, 0, st>>>(c, ring->idx, ring->rows);
+    gather_kernel<double><<<grid_for(ring->rows * W), 256, 0, st>>>(c, ring->idx, ring->cycle, ring->idx_stride,
+                                                                     ring->rows);
   }
   return check_launch("gather_kernel");
 }

@@ -106,6 +106,39 @@ __global__ void reduce_adam_kernel(const T* __restrict__ ws, int n, int64_t P, T
   }
 }
 
+template <typename T>
+__global__ void reduce_adam_graph_kernel(const T* __restrict__ ws, int n, int64_t P, T* p, T* m, T* v,
+                                         const int64_t* counter, const int64_t* step_base, const double* bc1,
+                                         const double* bc2, T lr, T b1, T b2, T eps, T one_m_b1, T one_m_b2, T* tgt,
+                                         T one_m_tau, T tau, T* loss_base) {
+  const int64_t c = *counter;
+  const int64_t t = *step_base + c + 1;
+  AdamK<T> k;
+  k.lr = lr;
+  k.b1 = b1;
+  k.b2 = b2;
+  k.eps = eps;
+  k.one_m_b1 = one_m_b1;
+  k.one_m_b2 = one_m_b2;
+  k.bc1 = (T)bc1[t];
+  k.bc2 = (T)bc2[t];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= P; i += (int64_t)gridDim.x * blockDim.x) {
+    T g = fold(ws, n, P + 1, i);
+    if (i == P) {
+      if (loss_base) loss_base[c] = g;
+      continue;
+    }
+    T pp = p[i], mm = m[i], vv = v[i];
+    adam_one(k, g, pp, mm, vv);
+    p[i] = pp;
+    m[i] = mm;
+    v[i] = vv;
+    if (tgt) tgt[i] = r_add(r_mul(one_m_tau, tgt[i]), r_mul(tau, pp));
+  }
+}
+
+__global__ void counter_tick_kernel(int64_t* c) { *c += 1; }
+
 static unsigned grid_of(int64_t P) {
   int64_t b = (P + 255) / 256;
   int64_t cap = 8 * (int64_t)num_sms();
@@ -173,4 +206,29 @@ extern "C" int cacto_reduce_adam(int32_t dtype, const void* workspace, int32_t n
         adam_consts<double>(step, lr, beta1, beta2, eps), (double*)target, 1.0 - tau, tau, (double*)grad_out,
         (double*)loss_out);
   return check_launch("reduce_adam_kernel");
+}
+
+extern "C" int cacto_reduce_adam_graph(int32_t dtype, const void* workspace, int32_t n_partials, int64_t P,
+                                       void* params, void* m, void* v, const int64_t* counter, const int64_t* step_base,
+                                       const double* bc1, const double* bc2, double lr, double beta1, double beta2,
+                                       double eps, void* target, double tau, void* loss_base, void* stream) {
+  if (!workspace || n_partials < 1 || P < 0 || !params || !m || !v || !counter || !step_base || !bc1 || !bc2)
+    return set_error(CACTO_EVALUE, "reduce_adam_graph: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CACTO_F32)
+    reduce_adam_graph_kernel<float><<<grid_of(P + 1), 256, 0, st>>>(
+        (const float*)workspace, n_partials, P, (float*)params, (float*)m, (float*)v, counter, step_base, bc1, bc2,
+        (float)lr, (float)beta1, (float)beta2, (float)eps, (float)(1.0 - beta1), (float)(1.0 - beta2),
+        (float*)target, (float)(1.0 - tau), (float)tau, (float*)loss_base);
+  else
+    reduce_adam_graph_kernel<double><<<grid_of(P + 1), 256, 0, st>>>(
+        (const double*)workspace, n_partials, P, (double*)params, (double*)m, (double*)v, counter, step_base, bc1,
+        bc2, lr, beta1, beta2, eps, 1.0 - beta1, 1.0 - beta2, (double*)target, 1.0 - tau, tau, (double*)loss_base);
+  return check_launch("reduce_adam_graph_kernel");
+}
+
+extern "C" int cacto_counter_tick(int64_t* counter, void* stream) {
+  if (!counter) return set_error(CACTO_EVALUE, "counter_tick: null counter");
+  counter_tick_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(counter);
+  return check_launch("counter_tick_kernel");
 }

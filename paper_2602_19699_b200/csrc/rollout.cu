@@ -8,8 +8,8 @@
 //   dynamics    x_s <- f(x_s, u_s), stage cost l(x_s, u_s) accumulated in the
 //               thread that owns start s, in NumPy's pairwise-sum order, so
 //               cost == Trajectory.cost (ilqr.py:76-78) term for term.
+#include "net.cuh"
 #include "systems.cuh"
-#include "tile.cuh"
 
 namespace cacto {
 
@@ -85,55 +85,30 @@ struct PairwiseSum {
   }
 };
 
+// S starts per CTA; TM = 8 (8x8 micro-tiles, 1 CTA / SM) for the 256-start
+// tile, TM = 4 otherwise
 template <typename T, int SYS, int HP, int S>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 2 : 1))
+__global__ void __launch_bounds__(kThreads, ((sizeof(T) == 4 && S <= 128) ? 2 : 1))
 rollout_kernel(const RolloutArgs<T> a) {
-  using TL = Tile<T, S, HP>;
+  using TL = Tile<T, S, HP, (S >= 256 ? 8 : 4)>;
   constexpr int n = SysDims<SYS>::n;
   constexpr int m = SysDims<SYS>::m;
   constexpr int IP = (n + 1) <= 8 ? 8 : ((n + 1) <= 16 ? 16 : 32);
-  const int nh = a.nh;
+  using NS = NetSmem<T, HP, IP, TL::KS>;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  // ---- carve shared memory -------------------------------------------------
-  T* W0 = sm;                         // [HP][IP] (or [m][IP] if nh == 0)
-  T* b0 = W0 + HP * IP;               // [HP]
-  T* Wh = b0 + HP;                    // (nh-1) x [HP][HP]
-  T* bh = Wh + (nh > 1 ? (nh - 1) : 0) * HP * HP;  // (nh-1) x [HP]
-  T* WL = bh + (nh > 1 ? (nh - 1) : 0) * HP;      // [m][HP]
-  T* bL = WL + m * HP;                // [m] (padded to 4)
-  T* A0 = bL + 4 * ((m + 3) / 4);     // [IP][S]
-  T* BA = A0 + IP * S;                // [HP][S]
-  T* BB = BA + HP * S;                // [HP][S]
-  T* US = BB + HP * S;                // [m][S] raw head outputs
-
-  // ---- stage weights (padded global layout -> swizzled smem) ------------------
-  {
-    const T* p = a.params;
-    if (nh == 0) {
-      stage_matrix(W0, p, m, IP);
-      stage_vector(bL, p + m * IP, m);
-    } else {
-      stage_matrix(W0, p, HP, IP);
-      p += HP * IP;
-      stage_vector(b0, p, HP);
-      p += HP;
-      for (int i = 0; i < nh - 1; ++i) {
-        stage_matrix(Wh + i * HP * HP, p, HP, HP);
-        p += HP * HP;
-        stage_vector(bh + i * HP, p, HP);
-        p += HP;
-      }
-      stage_matrix(WL, p, m, HP);
-      p += m * HP;
-      stage_vector(bL, p, m);
-    }
-  }
+  NS net;
+  T* A0 = net.carve(sm, a.nh, n + 1, m);  // [IP][S] input tile
+  T* BA = A0 + IP * S;                     // [HP][S]
+  T* BB = BA + HP * S;                     // [HP][S]
+  T* US = BB + HP * S;                     // [m][S] raw head outputs
+  net.stage(a.params);
   // zero the padded input rows once
   for (int p = threadIdx.x; p < IP * S; p += kThreads) A0[p] = T(0);
 
   // ---- per-start registers (thread s < S owns start s of this tile) ------------
+  static_assert(S <= kThreads, "one thread per start");
   const int s_own = threadIdx.x;
   const int64_t gi = (int64_t)blockIdx.x * S + s_own;
   const bool owner = s_own < S && gi < a.N;
@@ -163,8 +138,6 @@ rollout_kernel(const RolloutArgs<T> a) {
   const int kmax = s_kmax;
 
   const TL tl;
-  T accm[TL::TN][TL::TM];
-
   for (int k = 0; k < kmax; ++k) {
     // ---- normalised network input [x, t0 + k] (nets.py:416, 126-129) ----------
     if (owner) {
@@ -176,29 +149,8 @@ rollout_kernel(const RolloutArgs<T> a) {
       for (int c = 0; c <= n; ++c) A0[TL::at(c, s_own)] = T(0);
     }
     __syncthreads();
-    const T* cur = A0;
-    if (nh > 0) {
-      // layer 0: K = IP
-      tl.template gemm_fwd<IP>(W0, A0, accm);
-      tl.store(BA, accm, [&](T v, int r, int) { return act_value(a.act, v + b0[r]); });
-      __syncthreads();
-      cur = BA;
-      T* nxt = BB;
-      for (int i = 0; i < nh - 1; ++i) {
-        tl.template gemm_fwd<HP>(Wh + i * HP * HP, cur, accm);
-        const T* bi = bh + i * HP;
-        tl.store(nxt, accm, [&](T v, int r, int) { return act_value(a.act, v + bi[r]); });
-        __syncthreads();
-        T* t = const_cast<T*>(cur);
-        cur = nxt;
-        nxt = t;
-      }
-      TL::template narrow<HP>(cur, m, [&](int j, int kk) { return WL[swz<HP>(j, kk)]; },
-                              [&](int s, int j, T v) { US[j * S + s] = v + bL[j]; });
-    } else {
-      TL::template narrow<IP>(cur, m, [&](int j, int kk) { return W0[swz<IP>(j, kk)]; },
-                              [&](int s, int j, T v) { US[j * S + s] = v + bL[j]; });
-    }
+    const T* last = forward_hidden(tl, net, a.act, A0, BA, BB, (T*)nullptr);
+    forward_output<TL>(net, last, [&](int s, int j, T v) { US[j * S + s] = v; });
     __syncthreads();
     // ---- head, running cost, dynamics (thread per start) -----------------------
     if (owner && k < T_i) {
@@ -232,21 +184,34 @@ rollout_kernel(const RolloutArgs<T> a) {
   }
 }
 
-template <typename T, int SYS, int HP>
-static int launch_rollout(const RolloutArgs<T>& a, cudaStream_t st) {
-  constexpr int S = sizeof(T) == 4 ? 128 : 64;
+template <typename T, int SYS, int HP, int S>
+static int launch_rollout_s(const RolloutArgs<T>& a, cudaStream_t st) {
   constexpr int n = SysDims<SYS>::n, m = SysDims<SYS>::m;
   constexpr int IP = (n + 1) <= 8 ? 8 : ((n + 1) <= 16 ? 16 : 32);
-  int nhw = a.nh > 1 ? a.nh - 1 : 0;
-  size_t elems = (size_t)HP * IP + HP + (size_t)nhw * (HP * HP + HP) + (size_t)m * HP + 4 * ((m + 3) / 4) +
-                 (size_t)IP * S + 2 * (size_t)HP * S + (size_t)m * S;
+  using NS = NetSmem<T, HP, IP, Tile<T, S, HP, (S >= 256 ? 8 : 4)>::KS>;
+  size_t elems = NS::elems(a.nh, m) + (size_t)IP * S + 2 * (size_t)HP * S + (size_t)m * S;
   size_t bytes = elems * sizeof(T);
   auto kern = rollout_kernel<T, SYS, HP, S>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_ECUDA, "rollout: %zu B of shared memory not available", bytes);
   int64_t blocks = (a.N + S - 1) / S;
   kern<<<(unsigned)blocks, kThreads, bytes, st>>>(a);
   return check_launch("rollout_kernel");
+}
+
+// Tile size: 128 starts per CTA (2 CTAs / SM) when the batch fills the GPU,
+// 32-start tiles for small batches (e.g. the kept warm-start re-rollout) so
+// that the CTAs still cover every SM.
+template <typename T, int SYS, int HP>
+static int launch_rollout(const RolloutArgs<T>& a, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (a.N >= (int64_t)256 * num_sms() && HP == 64) return launch_rollout_s<T, SYS, HP, 256>(a, st);
+    if (a.N >= (int64_t)128 * num_sms()) return launch_rollout_s<T, SYS, HP, 128>(a, st);
+    return launch_rollout_s<T, SYS, HP, 32>(a, st);
+  } else {
+    if (a.N >= (int64_t)64 * num_sms()) return launch_rollout_s<T, SYS, HP, 64>(a, st);
+    return launch_rollout_s<T, SYS, HP, 32>(a, st);
+  }
 }
 
 template <typename T>

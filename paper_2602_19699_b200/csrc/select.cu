@@ -28,28 +28,29 @@ CACTO_D bool pair_less(const Pair& a, const Pair& b) {
   return a.key < b.key || (a.key == b.key && a.idx < b.idx);
 }
 
+// keys: NaN -> (max - 1), the max key is reserved for padding rows of merged runs
 CACTO_D unsigned long long score_key(float s) {
-  if (s != s) return 0xFFFFFFFFull;  // NaN last
+  if (s != s) return 0xFFFFFFFEull;  // NaN last
   if (s == 0.0f) s = 0.0f;           // -0.0 -> +0.0
   unsigned int b = __float_as_uint(s);
   unsigned int u = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
   return (unsigned long long)(~u);
 }
 CACTO_D unsigned long long score_key(double s) {
-  if (s != s) return 0xFFFFFFFFFFFFFFFFull;
+  if (s != s) return 0xFFFFFFFFFFFFFFFEull;
   if (s == 0.0) s = 0.0;
   unsigned long long b = (unsigned long long)__double_as_longlong(s);
   unsigned long long u = (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
   return ~u;
 }
 CACTO_D float key_score(unsigned long long k, float*) {
-  if (k == 0xFFFFFFFFull) return __uint_as_float(0x7fc00000u);
+  if (k >= 0xFFFFFFFEull) return __uint_as_float(0x7fc00000u);
   unsigned int u = ~(unsigned int)k;
   unsigned int b = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
   return __uint_as_float(b);
 }
 CACTO_D double key_score(unsigned long long k, double*) {
-  if (k == 0xFFFFFFFFFFFFFFFFull) return __longlong_as_double(0x7ff8000000000000ll);
+  if (k >= 0xFFFFFFFFFFFFFFFEull) return __longlong_as_double(0x7ff8000000000000ll);
   unsigned long long u = ~k;
   unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7FFFFFFFFFFFFFFFull) : ~u;
   return __longlong_as_double((long long)b);
@@ -241,7 +242,7 @@ __global__ void emit_kernel(const Pair* __restrict__ sel, int64_t keep, int64_t 
 template <typename T>
 __global__ void runs_to_pairs_kernel(const T* __restrict__ s, const int64_t* __restrict__ idx, int64_t M, Pair* out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = Pair{score_key(s[i]), (long long)idx[i]};
+    out[i] = Pair{idx[i] < 0 ? ~0ull : score_key(s[i]), (long long)idx[i]};  // idx < 0: padding
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }

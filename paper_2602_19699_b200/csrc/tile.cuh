@@ -1,50 +1,57 @@
 // tile.cuh -- shared-memory tile engine for the fused small-MLP kernels.
 //
 // A CTA of 256 threads owns a tile of S samples.  Activations live in shared
-// memory "unit-major": tile[r][s] (row r = unit / feature, s = sample), with an
-// XOR swizzle on 4-element chunks so that both the GEMM inner loops (a warp
-// reads 4 distinct sample-chunks of one row) and the epilogue stores (a warp
-// writes 8 rows x 4 chunks) are bank-conflict free.  Weights are staged once
-// per CTA in shared memory in the reference row-major layout W[out][in]
-// (nets.py:116), swizzled the same way; ONE copy serves the forward GEMMs
-// (z = a W^T, reading 4 consecutive k of a row) and the backward GEMMs
-// (s = g W, reading TN consecutive in-units of a row).
+// memory "unit-major": tile[r][s] (row r = unit / feature, s = sample).  Weights
+// are staged once per CTA in the reference row-major layout W[out][in]
+// (nets.py:116); ONE copy serves the forward GEMMs (z = a W^T: a thread reads 4
+// consecutive k of its unit rows) and the backward GEMMs (s = g W: a thread
+// reads its TN consecutive in-units of one row).
 //
-// Register micro-tile: each thread owns TM=4 samples x TN units (TN = HP/TX).
+// Register micro-tile: each thread owns TM = 4 samples x TN = HP/TX units,
+// units contiguous (rows tx*TN .. tx*TN+TN-1).  Every [rows][C] array is XOR
+// swizzled on 16-byte chunks with the key (row >> KS) & 7, KS = log2(TN): the
+// 8 threads of a warp that read 8 different unit rows at the same logical
+// chunk then hit 8 different bank groups (conflict-free), and epilogue stores
+// (8 rows x 4 sample chunks per warp) take the minimum 4 wavefronts.  All
+// addressing is hoisted: per 4-k chunk a thread does one XOR for its weight
+// rows and one for its sample chunk.
 #pragma once
 
 #include "common.cuh"
 
 namespace cacto {
 
-// swizzled index of element (r, c) in a row-major [*][C] array (C % 4 == 0,
-// C/4 a power of two)
-template <int C>
+constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+
+// swizzled index of element (r, c) in a row-major [*][C] array; C % 4 == 0 and
+// C/4 a power of two; KS = key shift
+template <int C, int KS>
 CACTO_HD int swz(int r, int c) {
   constexpr int NCH = C / 4;
   constexpr int KM = (NCH >= 8 ? 8 : NCH) - 1;
-  return r * C + ((((c >> 2) ^ ((r >> 2) & KM))) << 2) + (c & 3);
+  return r * C + ((((c >> 2) ^ ((r >> KS) & KM))) << 2) + (c & 3);
 }
 
-// runtime-C variant (C in {8, 16, 32, 64, 128})
-CACTO_HD int swz_rt(int C, int r, int c) {
-  int nch = C >> 2;
-  int km = (nch >= 8 ? 8 : nch) - 1;
-  return r * C + ((((c >> 2) ^ ((r >> 2) & km))) << 2) + (c & 3);
-}
+// stride of the first layer's weight rows in shared memory: at least 32 columns
+// so that the XOR key has 8 chunk positions (rows are only IP = 8..32 wide)
+template <int IP>
+constexpr int w0_stride() { return IP < 32 ? 32 : IP; }
 
-template <typename T, int S, int HP>
+template <typename T, int S, int HP, int TM_ = 4>
 struct Tile {
-  static constexpr int TM = 4;
+  static constexpr int TM = TM_;  // samples per thread: 4 or 8 (1 or 2 16-byte chunks)
+  static constexpr int TC = TM / 4;
   static constexpr int TY = S / TM;
   static constexpr int TX = kThreads / TY;
   static constexpr int TN = HP / TX;
+  static constexpr int KS = ilog2(TN);
   static_assert(TY * TX == kThreads, "tile/thread mismatch");
-  static_assert(TN >= 1 && TN * TX == HP, "hidden width must split over TX");
+  static_assert(TM == 4 || TM == 8, "TM must be 4 or 8");
+  static_assert(TN >= 1 && TN * TX == HP && (1 << KS) == TN, "hidden width must split over TX");
   static constexpr int LX = TX < 8 ? TX : 8;
   static constexpr int LY = 32 / LX;
   static constexpr int WX = TX / LX;
-  static constexpr int ELEMS = HP * S;  // elements of one [HP][S] tile
+  static constexpr int KMS = (S / 4 >= 8 ? 8 : S / 4) - 1;  // key mask of activation tiles
 
   int tx, ty;
 
@@ -54,28 +61,43 @@ struct Tile {
     ty = (warp / WX) * LY + (lane / LX);
   }
 
-  CACTO_D static int at(int r, int s) { return swz<S>(r, s); }
+  // activation tile [rows][S]
+  CACTO_HD static int at(int r, int s) { return swz<S, KS>(r, s); }
+  // weight matrix with row stride C
+  template <int C>
+  CACTO_HD static int wat(int r, int c) { return swz<C, KS>(r, c); }
 
-  // acc[j][i] = sum_k A[k][s_i] * W[n_j][k]   (W swizzled, row length K)
-  template <int K>
+  // acc[j][i] = sum_{k<K} A[k][s_i] * W[n_j][k]   (W rows of stride WC, swizzled)
+  template <int K, int WC>
   CACTO_D void gemm_fwd(const T* __restrict__ W, const T* __restrict__ A, T (&acc)[TN][TM]) const {
+    constexpr int KMW = (WC / 4 >= 8 ? 8 : WC / 4) - 1;
+    constexpr uint32_t ES = sizeof(T);
 #pragma unroll
     for (int j = 0; j < TN; ++j)
 #pragma unroll
       for (int i = 0; i < TM; ++i) acc[j][i] = T(0);
-#pragma unroll 2
+    const uint32_t wrow = saddr(W) + (uint32_t)(tx * TN * WC) * ES;
+    const uint32_t abase = saddr(A);
+    const int wkey = tx & KMW;  // (tx*TN + j) >> KS == tx for every j < TN
+#pragma unroll 4
     for (int kc = 0; kc < K / 4; ++kc) {
       T a[4][TM];
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        V4<T> v = ld4(A + swz<S>(4 * kc + kk, ty * TM));
+        const int r = 4 * kc + kk;
+        const int key = (r >> KS) & KMS;  // uniform over the warp
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[kk][i] = v.v[i];
+        for (int h = 0; h < TC; ++h) {
+          V4<T> v = lds4(abase + (uint32_t)(r * S + (((ty * TC + h) ^ key) << 2)) * ES, (T*)nullptr);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a[kk][4 * h + e] = v.v[e];
+        }
       }
+      const uint32_t wc = wrow + (uint32_t)((kc ^ wkey) << 2) * ES;
       T w[TN][4];
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
-        V4<T> v = ld4(W + swz<K>(tx * TN + j, 4 * kc));
+        V4<T> v = lds4(wc + j * WC * ES, (T*)nullptr);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) w[j][kk] = v.v[kk];
       }
@@ -88,44 +110,64 @@ struct Tile {
     }
   }
 
-  // acc[j][i] = sum_{o<K} A[o][s_i] * W[o][n_j]   (W [K][HP] swizzled; K runtime)
+  // acc[j][i] = sum_{o<K} A[o][s_i] * W[o][n_j]   (W [K][HP], stride HP; K runtime)
   CACTO_D void gemm_bwd(const T* __restrict__ W, const T* __restrict__ A, int K, T (&acc)[TN][TM]) const {
+    constexpr int KMW = (HP / 4 >= 8 ? 8 : HP / 4) - 1;
+    constexpr uint32_t ES = sizeof(T);
 #pragma unroll
     for (int j = 0; j < TN; ++j)
 #pragma unroll
       for (int i = 0; i < TM; ++i) acc[j][i] = T(0);
+    const uint32_t abase = saddr(A), wbase = saddr(W);
 #pragma unroll 4
     for (int o = 0; o < K; ++o) {
-      V4<T> a = ld4(A + swz<S>(o, ty * TM));
+      T a[TM];
+#pragma unroll
+      for (int h = 0; h < TC; ++h) {
+        V4<T> v = lds4(abase + (uint32_t)(o * S + (((ty * TC + h) ^ ((o >> KS) & KMS)) << 2)) * ES, (T*)nullptr);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a[4 * h + e] = v.v[e];
+      }
+      const int wk = (o >> KS) & KMW;
+      const uint32_t wr = wbase + (uint32_t)(o * HP) * ES;
       T w[TN];
       if constexpr (TN % 4 == 0) {
 #pragma unroll
         for (int q = 0; q < TN / 4; ++q) {
-          V4<T> v = ld4(W + swz<HP>(o, tx * TN + 4 * q));
+          V4<T> v = lds4(wr + (uint32_t)((((tx * TN) / 4 + q) ^ wk) << 2) * ES, (T*)nullptr);
 #pragma unroll
           for (int e = 0; e < 4; ++e) w[4 * q + e] = v.v[e];
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < TN; ++j) w[j] = W[swz<HP>(o, tx * TN + j)];
+        for (int j = 0; j < TN; ++j) {
+          const int n = tx * TN + j;
+          w[j] = lds1(wr + (uint32_t)((((n >> 2) ^ wk) << 2) + (n & 3)) * ES, (T*)nullptr);
+        }
       }
 #pragma unroll
       for (int j = 0; j < TN; ++j)
 #pragma unroll
-        for (int i = 0; i < TM; ++i) acc[j][i] = fma(a.v[i], w[j], acc[j][i]);
+        for (int i = 0; i < TM; ++i) acc[j][i] = fma(a[i], w[j], acc[j][i]);
     }
   }
 
   // out[n_j][s_i] = f(acc[j][i], n_j, s_i) for the thread's micro-tile
   template <typename F>
   CACTO_D void store(T* __restrict__ out, const T (&acc)[TN][TM], F f) const {
+    constexpr uint32_t ES = sizeof(T);
+    const uint32_t ob = saddr(out) + (uint32_t)(tx * TN * S) * ES;
+    const int key = tx & KMS;  // row key of every row tx*TN + j
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       int r = tx * TN + j;
-      V4<T> v;
 #pragma unroll
-      for (int i = 0; i < TM; ++i) v.v[i] = f(acc[j][i], r, ty * TM + i);
-      st4(out + swz<S>(r, ty * TM), v);
+      for (int h = 0; h < TC; ++h) {
+        V4<T> v;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v.v[e] = f(acc[j][4 * h + e], r, ty * TM + 4 * h + e);
+        sts4(ob + (uint32_t)(j * S + (((ty * TC + h) ^ key) << 2)) * ES, v);
+      }
     }
   }
 
@@ -141,8 +183,10 @@ struct Tile {
       int s = p % S, j = p / S;
       T sum = T(0);
       if (live) {
+        const uint32_t ab = saddr(A);
 #pragma unroll 4
-        for (int k = q * (K / 4); k < (q + 1) * (K / 4); ++k) sum = fma(A[swz<S>(k, s)], w(j, k), sum);
+        for (int k = q * (K / 4); k < (q + 1) * (K / 4); ++k)
+          sum = fma(lds1(ab + (uint32_t)at(k, s) * (uint32_t)sizeof(T), (T*)nullptr), w(j, k), sum);
       }
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
@@ -155,18 +199,26 @@ struct Tile {
   CACTO_D static void each(int R, F f) {
     for (int p = threadIdx.x; p < R * S; p += kThreads) {
       int r = p / S, s = p % S;
-      f(r, s, swz<S>(r, s));
+      f(r, s, at(r, s));
     }
   }
 };
 
-// load a padded row-major [rows][cols] global matrix into swizzled shared memory
+// runtime swizzle (staging): row length C in {8..128}, key shift KS
+CACTO_HD int swz_rt(int C, int KS, int r, int c) {
+  int nch = C >> 2;
+  int km = (nch >= 8 ? 8 : nch) - 1;
+  return r * C + ((((c >> 2) ^ ((r >> KS) & km))) << 2) + (c & 3);
+}
+
+// load a padded row-major [rows][cols] global matrix into shared memory rows of
+// stride `stride` (>= cols), swizzled with key shift KS
 template <typename T>
-CACTO_D void stage_matrix(T* __restrict__ dst, const T* __restrict__ src, int rows, int cols) {
-  int nch = rows * cols / 4;
+CACTO_D void stage_matrix(T* __restrict__ dst, const T* __restrict__ src, int rows, int cols, int stride, int KS) {
+  int cq = cols / 4, nch = rows * cq;
   for (int q = threadIdx.x; q < nch; q += kThreads) {
-    int r = (q * 4) / cols, c = (q * 4) % cols;
-    st4(dst + swz_rt(cols, r, c), ld4(src + (int64_t)q * 4));
+    int r = q / cq, c = (q % cq) * 4;
+    st4(dst + swz_rt(stride, KS, r, c), ld4(src + (int64_t)r * cols + c));
   }
 }
 template <typename T>

@@ -22,16 +22,23 @@ namespace cacto {
 template <typename T>
 struct BatchDev {
   const int64_t* idx;
+  const int64_t* cycle;
+  int64_t idx_stride;
   const T *xa, *u, *v_bar, *v_bar_x, *xa_plus_k;
   int64_t rows;
   int n, m, t_max;
-  CACTO_D int64_t row(int64_t b) const { return idx ? idx[b] : b; }
+  CACTO_D int64_t row(int64_t b) const {
+    if (!idx) return b;
+    return cycle ? idx[(*cycle) * idx_stride + b] : idx[b];
+  }
 };
 
 template <typename T>
 BatchDev<T> batch_dev(const cacto_batch_t& b) {
   BatchDev<T> d;
   d.idx = b.idx;
+  d.cycle = b.cycle;
+  d.idx_stride = b.idx_stride;
   d.xa = (const T*)b.xa;
   d.u = (const T*)b.u;
   d.v_bar = (const T*)b.v_bar;
@@ -46,8 +53,9 @@ BatchDev<T> batch_dev(const cacto_batch_t& b) {
 
 // ---- gradient-slot accumulation helpers (slot is this CTA's private region) -----
 // g[r][c] += sum_s A[r][s] * B[c][s]  (R, C multiples of 4; A, B swizzled tiles)
-template <typename T, int S>
+template <typename TL, typename T>
 CACTO_D void outer_acc4(T* __restrict__ g, int R, int C, const T* __restrict__ A, const T* __restrict__ B) {
+  constexpr int S = TL::TY * TL::TM;
   const int cb = C / 4, nblk = (R / 4) * cb;
   for (int blk = threadIdx.x; blk < nblk; blk += kThreads) {
     int r0 = (blk / cb) * 4, c0 = (blk % cb) * 4;
@@ -57,8 +65,8 @@ CACTO_D void outer_acc4(T* __restrict__ g, int R, int C, const T* __restrict__ A
       V4<T> a[4], b[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        a[j] = ld4(A + swz<S>(r0 + j, 4 * sc));
-        b[j] = ld4(B + swz<S>(c0 + j, 4 * sc));
+        a[j] = ld4(A + TL::at(r0 + j, 4 * sc));
+        b[j] = ld4(B + TL::at(c0 + j, 4 * sc));
       }
 #pragma unroll
       for (int jr = 0; jr < 4; ++jr)
@@ -74,17 +82,18 @@ CACTO_D void outer_acc4(T* __restrict__ g, int R, int C, const T* __restrict__ A
   }
 }
 // same with 1-row blocks (any R)
-template <typename T, int S>
+template <typename TL, typename T>
 CACTO_D void outer_acc1(T* __restrict__ g, int R, int C, const T* __restrict__ A, const T* __restrict__ B) {
+  constexpr int S = TL::TY * TL::TM;
   const int cb = C / 4, nblk = R * cb;
   for (int blk = threadIdx.x; blk < nblk; blk += kThreads) {
     int r0 = blk / cb, c0 = (blk % cb) * 4;
     T acc[4] = {};
     for (int sc = 0; sc < S / 4; ++sc) {
-      V4<T> a = ld4(A + swz<S>(r0, 4 * sc));
+      V4<T> a = ld4(A + TL::at(r0, 4 * sc));
 #pragma unroll
       for (int jc = 0; jc < 4; ++jc) {
-        V4<T> b = ld4(B + swz<S>(c0 + jc, 4 * sc));
+        V4<T> b = ld4(B + TL::at(c0 + jc, 4 * sc));
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[jc] = fma(a.v[e], b.v[e], acc[jc]);
       }
@@ -94,12 +103,13 @@ CACTO_D void outer_acc1(T* __restrict__ g, int R, int C, const T* __restrict__ A
   }
 }
 // g[r] += sum_s A[r][s]
-template <typename T, int S>
+template <typename TL, typename T>
 CACTO_D void rowsum_acc(T* __restrict__ g, int R, const T* __restrict__ A) {
+  constexpr int S = TL::TY * TL::TM;
   for (int r = threadIdx.x; r < R; r += kThreads) {
     T acc = T(0);
     for (int sc = 0; sc < S / 4; ++sc) {
-      V4<T> a = ld4(A + swz<S>(r, 4 * sc));
+      V4<T> a = ld4(A + TL::at(r, 4 * sc));
       acc += (a.v[0] + a.v[1]) + (a.v[2] + a.v[3]);
     }
     g[r] += acc;
@@ -166,22 +176,17 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  NetSm<T, HP, IP> net;
+  NetSmem<T, HP, IP, TL::KS> net;
   T* p = net.carve(sm, a.nh, a.in, 1);
   T* A0 = p;
   p += IP * S;
   T* U0 = p;
   p += IP * S;
-  T* Z[CACTO_MAX_LAYERS];
-  T* G[CACTO_MAX_LAYERS];
-  for (int i = 0; i < a.nh; ++i) {
-    Z[i] = p;
-    p += HP * S;
-  }
-  for (int i = 0; i < a.nh; ++i) {
-    G[i] = p;
-    p += HP * S;
-  }
+  constexpr int TS = HP * S;  // elements per [HP][S] tile
+  T* const Zb = p;            // z_i tiles (consecutive)
+  p += (size_t)a.nh * TS;
+  T* const Gb = p;            // g_i -> zeta_i -> zbar_i tiles
+  p += (size_t)a.nh * TS;
   T* P = p;
   p += HP * S;
   T* Q = p;
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
   const int64_t ntiles = (a.b.rows + S - 1) / S;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t base = t * S;
-    load_input_tile<T, S>(A0, IP, a.in, a.nc,
+    load_input_tile<TL>(A0, IP, a.in, a.nc,
                           [&](int s) { return base + s < a.b.rows ? a.b.row(base + s) : (int64_t)-1; },
                           [&](int64_t r, int c) { return a.b.xa[r * a.in + c]; });
     for (int s = threadIdx.x; s < S; s += kThreads) {
@@ -217,13 +222,13 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
       EV[s] = y;
     }
     __syncthreads();
-    const T* last = forward_hidden<T, S, HP, IP>(tl, net, a.act, A0, P, Q, Z);
-    forward_output<T, S, HP, IP>(net, last, [&](int s, int, T o) {
+    const T* last = forward_hidden(tl, net, a.act, A0, P, Q, Zb);
+    forward_output<TL>(net, last, [&](int s, int, T o) {
       EV[s] = (base + s < a.b.rows) ? EV[s] - o : T(0);  // e_v = y - V
     });
     __syncthreads();
     // input-gradient sweep -> e_g = v_bar_x - dV/dx[:n]  (nets.py:258-270)
-    input_grad_sweep<T, S, HP, IP>(tl, net, a.act, 0, Z, G, P, Q, [&](int s, int c, T v) {
+    input_grad_sweep(tl, net, a.act, 0, Zb, Gb, P, Q, [&](int s, int c, T v) {
       if (c < n) {
         T e = T(0);
         if (base + s < a.b.rows) e = a.b.v_bar_x[a.b.row(base + s) * n + c] - v / a.nc.in_half[c];
@@ -255,15 +260,15 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
     T accm[TL::TN][TL::TM];
     for (int i = 0; i < nh; ++i) {
       if (i == 0)
-        tl.template gemm_fwd<IP>(net.W[0], u, accm);
+        tl.template gemm_fwd<IP, decltype(net)::W0S>(net.W(0), u, accm);
       else
-        tl.template gemm_fwd<HP>(net.W[i], u, accm);
+        tl.template gemm_fwd<HP, HP>(net.W(i), u, accm);
       tl.store(rb, accm, [](T v, int, int) { return v; });
-      outer_acc4<T, S>(slot + a.off.w[i], HP, i == 0 ? IP : HP, G[i], u);  // (d1 * s)^T u
+      outer_acc4<TL>(slot + a.off.w[i], HP, i == 0 ? IP : HP, (Gb + (i) * TS), u);  // (d1 * s)^T u
       __syncthreads();
       {
-        const T* z = Z[i];
-        T* g = G[i];
+        const T* z = (Zb + (i) * TS);
+        T* g = (Gb + (i) * TS);
         TL::each(HP, [&](int, int, int q) {
           T zz = z[q], r = rb[q];
           g[q] = act_h(a.act, zz) * g[q] * r;  // zeta_i = act''(z) s rbar
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
       u = rb;
       rb = (rb == Q) ? P : Q;
     }
-    rowsum_acc<T, S>(slot + a.off.w[L1], KL, u);  // grads[2*last] += u.sum(0)
+    rowsum_acc<TL>(slot + a.off.w[L1], KL, u);  // grads[2*last] += u.sum(0)
     // value path (nets.py:287-289, 215-230)
     for (int s = threadIdx.x; s < S; s += kThreads) EV[s] = T(-2) * a.inv_denom * EV[s];  // delta
     __syncthreads();
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
       const T* aL = A0;
       if (nh > 0) {
         T* dst = (u == P) ? Q : P;  // a buffer not holding u
-        const T* z = Z[nh - 1];
+        const T* z = (Zb + (nh - 1) * TS);
         TL::each(HP, [&](int, int, int q) { dst[q] = act_value(a.act, z[q]); });
         __syncthreads();
         aL = dst;
@@ -303,24 +308,23 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
     if (nh > 0) {
       T* AB = P;  // abar
       T* AS = Q;  // a_i scratch
-      const T* WL = net.W[L1];
-      TL::each(HP, [&](int r, int s, int q) { AB[q] = EV[s] * WL[swz<HP>(0, r)]; });
+      TL::each(HP, [&](int r, int s, int q) { AB[q] = EV[s] * net.w(L1, 0, r); });
       __syncthreads();
       for (int i = nh - 1; i >= 0; --i) {
         {
-          const T* z = Z[i];
-          T* g = G[i];
+          const T* z = (Zb + (i) * TS);
+          T* g = (Gb + (i) * TS);
           TL::each(HP, [&](int, int, int q) { g[q] = act_d1(a.act, z[q]) * AB[q] + g[q]; });  // zbar_i
         }
         if (i > 0) {
-          const T* z = Z[i - 1];
+          const T* z = (Zb + (i - 1) * TS);
           TL::each(HP, [&](int, int, int q) { AS[q] = act_value(a.act, z[q]); });
         }
         __syncthreads();
-        rowsum_acc<T, S>(slot + a.off.b[i], HP, G[i]);
-        outer_acc4<T, S>(slot + a.off.w[i], HP, i == 0 ? IP : HP, G[i], i == 0 ? A0 : AS);
+        rowsum_acc<TL>(slot + a.off.b[i], HP, (Gb + (i) * TS));
+        outer_acc4<TL>(slot + a.off.w[i], HP, i == 0 ? IP : HP, (Gb + (i) * TS), i == 0 ? A0 : AS);
         if (i > 0) {
-          tl.gemm_bwd(net.W[i], G[i], HP, accm);
+          tl.gemm_bwd(net.W(i), (Gb + (i) * TS), HP, accm);
           __syncthreads();  // AS / AB reads of this layer are complete
           tl.store(AB, accm, [](T v, int, int) { return v; });
         }
@@ -363,15 +367,13 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  NetSm<T, HP, IP> net;
+  NetSmem<T, HP, IP, TL::KS> net;
   T* p = net.carve(sm, a.nh, a.in, a.out);
   T* A0 = p;
   p += IP * S;
-  T* Z[CACTO_MAX_LAYERS];
-  for (int i = 0; i < a.nh; ++i) {
-    Z[i] = p;
-    p += HP * S;
-  }
+  constexpr int TS = HP * S;
+  T* const Zb = p;  // z_i tiles (consecutive), overwritten by zbar_i in the backward pass
+  p += (size_t)a.nh * TS;
   T* P = p;
   p += HP * S;
   T* Q = p;
@@ -394,12 +396,12 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
   T accm[TL::TN][TL::TM];
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t base = t * S;
-    load_input_tile<T, S>(A0, IP, a.in, a.nc,
+    load_input_tile<TL>(A0, IP, a.in, a.nc,
                           [&](int s) { return base + s < a.b.rows ? a.b.row(base + s) : (int64_t)-1; },
                           [&](int64_t r, int c) { return a.b.xa[r * a.in + c]; });
     __syncthreads();
-    const T* last = forward_hidden<T, S, HP, IP>(tl, net, a.act, A0, P, Q, Z);
-    forward_output<T, S, HP, IP>(net, last, [&](int s, int j, T o) { OUT[j * S + s] = o; });
+    const T* last = forward_hidden(tl, net, a.act, A0, P, Q, Zb);
+    forward_output<TL>(net, last, [&](int s, int j, T o) { OUT[j * S + s] = o; });
     __syncthreads();
     // per-sample output cotangent + loss term
     T term = T(0);
@@ -439,29 +441,29 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
           }
         }
       }
-      for (int j = 0; j < out; ++j) DEL[swz<S>(j, s)] = d[j];
+      for (int j = 0; j < out; ++j) DEL[TL::at(j, s)] = d[j];
     }
     block_add(term, slot + P_total);  // (contains __syncthreads)
     // output layer: gW_L += DEL^T a_L ; gb_L += rowsum(DEL)
     const T* aL = A0;
     if (nh > 0) {
-      const T* z = Z[nh - 1];
+      const T* z = (Zb + (nh - 1) * TS);
       TL::each(HP, [&](int, int, int q) { P[q] = act_value(a.act, z[q]); });
       __syncthreads();
       aL = P;
     }
-    outer_acc1<T, S>(slot + a.off.w[L1], out, KL, DEL, aL);
-    rowsum_acc<T, S>(slot + a.off.b[L1], out, DEL);
+    outer_acc1<TL>(slot + a.off.w[L1], out, KL, DEL, aL);
+    rowsum_acc<TL>(slot + a.off.b[L1], out, DEL);
     if (nh > 0) {
       // abar = DEL W_L
-      tl.gemm_bwd(net.W[L1], DEL, out, accm);
+      tl.gemm_bwd(net.W(L1), DEL, out, accm);
       __syncthreads();
       tl.store(Q, accm, [](T v, int, int) { return v; });
       __syncthreads();
       for (int i = nh - 1; i >= 0; --i) {
-        T* zb = Z[i];
+        T* zb = (Zb + (i) * TS);
         if (i > 0) {
-          const T* zp = Z[i - 1];
+          const T* zp = (Zb + (i - 1) * TS);
           TL::each(HP, [&](int, int, int q) {
             zb[q] = act_d1(a.act, zb[q]) * Q[q];  // zbar_i (overwrites z_i)
             P[q] = act_value(a.act, zp[q]);       // a_i
@@ -470,10 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
           TL::each(HP, [&](int, int, int q) { zb[q] = act_d1(a.act, zb[q]) * Q[q]; });
         }
         __syncthreads();
-        rowsum_acc<T, S>(slot + a.off.b[i], HP, zb);
-        outer_acc4<T, S>(slot + a.off.w[i], HP, i == 0 ? IP : HP, zb, i == 0 ? A0 : P);
+        rowsum_acc<TL>(slot + a.off.b[i], HP, zb);
+        outer_acc4<TL>(slot + a.off.w[i], HP, i == 0 ? IP : HP, zb, i == 0 ? A0 : P);
         if (i > 0) {
-          tl.gemm_bwd(net.W[i], zb, HP, accm);
+          tl.gemm_bwd(net.W(i), zb, HP, accm);
           __syncthreads();
           tl.store(Q, accm, [](T v, int, int) { return v; });
         }
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(kThreads) actor_prep_kernel(const PrepArgs<T> 
   constexpr int nn = SysDims<SYS>::n, mm = SysDims<SYS>::m;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  NetSm<T, HP, IP> net;
+  NetSmem<T, HP, IP, TL::KS> net;
   T* p = net.carve(sm, a.nh, a.in, a.out);
   T* A0 = p;
   T* P0 = A0 + IP * S;
@@ -515,12 +517,12 @@ __global__ void __launch_bounds__(kThreads) actor_prep_kernel(const PrepArgs<T> 
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t base = t * S;
     __syncthreads();
-    load_input_tile<T, S>(A0, IP, a.in, a.nc,
+    load_input_tile<TL>(A0, IP, a.in, a.nc,
                           [&](int s) { return base + s < a.b.rows ? a.b.row(base + s) : (int64_t)-1; },
                           [&](int64_t r, int c) { return a.b.xa[r * a.in + c]; });
     __syncthreads();
-    const T* last = forward_hidden<T, S, HP, IP>(tl, net, a.act, A0, P0, P1, nullptr);
-    forward_output<T, S, HP, IP>(net, last, [&](int s, int j, T o) { OUT[j * S + s] = o; });
+    const T* last = forward_hidden(tl, net, a.act, A0, P0, P1, (T*)nullptr);
+    forward_output<TL>(net, last, [&](int s, int j, T o) { OUT[j * S + s] = o; });
     __syncthreads();
     for (int s = threadIdx.x; s < S; s += kThreads) {
       if (base + s >= a.b.rows) continue;
@@ -540,11 +542,12 @@ __global__ void __launch_bounds__(kThreads) actor_prep_kernel(const PrepArgs<T> 
   }
 }
 
-__global__ void count_live_kernel(const int64_t* idx, const void* xa, int dtype, int64_t rows, int n, int t_max,
-                                  int64_t* out) {
+__global__ void count_live_kernel(const int64_t* idx, const int64_t* cycle, int64_t stride, const void* xa, int dtype,
+                                  int64_t rows, int n, int t_max, int64_t* out) {
   __shared__ unsigned long long acc;
   if (threadIdx.x == 0) acc = 0;
   __syncthreads();
+  if (idx && cycle) idx += (*cycle) * stride;
   unsigned long long c = 0;
   for (int64_t b = threadIdx.x; b < rows; b += blockDim.x) {
     int64_t r = idx ? idx[b] : b;
@@ -595,11 +598,11 @@ static void* scratch_of(const cacto_mlp_t* net, void* ws) {
 template <typename T, int HP, int IP>
 static int launch_critic(const CriticArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
   constexpr int S = critic_S<T>();
-  size_t el = NetSm<T, HP, IP>::elems(a.nh, 1) + 2 * (size_t)IP * S + (2 * (size_t)a.nh + 2) * HP * S + S +
+  size_t el = net_elems<T, HP, IP>(a.nh, 1) + 2 * (size_t)IP * S + (2 * (size_t)a.nh + 2) * HP * S + S +
               (size_t)CACTO_MAX_IN * S;
   size_t bytes = el * sizeof(T);
   auto kern = critic_kernel<T, HP, IP, S>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_EUNSUPPORTED, "critic_loss: %zu B shared memory not available", bytes);
   int grid = loss_grid(rows, S);
   kern<<<grid, kThreads, bytes, st>>>(a);
@@ -660,11 +663,11 @@ extern "C" int cacto_critic_loss(const cacto_mlp_t* critic, const cacto_mlp_t* t
 template <typename T, int HP, int IP, int KIND, int SYS>
 static int launch_vp(const VpArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
   constexpr int S = critic_S<T>();
-  size_t el = NetSm<T, HP, IP>::elems(a.nh, a.out) + (size_t)IP * S + ((size_t)a.nh + 2) * HP * S +
+  size_t el = net_elems<T, HP, IP>(a.nh, a.out) + (size_t)IP * S + ((size_t)a.nh + 2) * HP * S +
               (size_t)CACTO_MAX_OUT * S + 4 * ((CACTO_MAX_OUT + 3) / 4) * S;
   size_t bytes = el * sizeof(T);
   auto kern = vp_kernel<T, HP, IP, S, KIND, SYS>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_EUNSUPPORTED, "loss: %zu B shared memory not available", bytes);
   int grid = loss_grid(rows, S);
   kern<<<grid, kThreads, bytes, st>>>(a);
@@ -728,10 +731,10 @@ extern "C" int cacto_std_loss(const cacto_mlp_t* std_net, const cacto_mlp_t* cri
 template <typename T, int HP, int IP, int SYS>
 static int launch_prep(const PrepArgs<T>& a, cudaStream_t st) {
   constexpr int S = 64;
-  size_t el = NetSm<T, HP, IP>::elems(a.nh, a.out) + (size_t)IP * S + 2 * (size_t)HP * S + (size_t)CACTO_MAX_OUT * S;
+  size_t el = net_elems<T, HP, IP>(a.nh, a.out) + (size_t)IP * S + 2 * (size_t)HP * S + (size_t)CACTO_MAX_OUT * S;
   size_t bytes = el * sizeof(T);
   auto kern = actor_prep_kernel<T, HP, IP, S, SYS>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_EUNSUPPORTED, "actor_prep: %zu B shared memory not available", bytes);
   int64_t tiles = (a.b.rows + S - 1) / S;
   int grid = (int)(tiles < 2 * num_sms() ? tiles : 2 * num_sms());
@@ -826,7 +829,7 @@ extern "C" int cacto_actor_loss(const cacto_mlp_t* actor, const cacto_mlp_t* cri
 
 extern "C" int cacto_count_live(const cacto_batch_t* batch, int64_t* live_rows, void* stream) {
   if (!batch || !live_rows) return set_error(CACTO_EVALUE, "count_live: null argument");
-  count_live_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(batch->idx, batch->xa, batch->dtype, batch->rows, batch->n,
-                                                         batch->t_max, live_rows);
+  count_live_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(batch->idx, batch->cycle, batch->idx_stride, batch->xa,
+                                                         batch->dtype, batch->rows, batch->n, batch->t_max, live_rows);
   return check_launch("count_live_kernel");
 }

@@ -1,0 +1,216 @@
+"""Device-resident network-update loop (reference trainer.py:208-234).
+
+Per iteration the reference runs M cycles of
+    minibatch -> critic_loss -> adam -> polyak(target) -> actor_loss(updated critic) -> adam
+and then M std-critic cycles, every minibatch drawn from one NumPy Generator
+(`rng_batches`, trainer.py:123) over a replay buffer that does not change
+during the loop.  `UpdateEngine` keeps the four networks, their Adam moments
+and the replay ring in HBM, draws the SAME 2*M index lists from the
+reference's generator up front (one H2D copy), and replays two captured CUDA
+graphs -- one critic+actor cycle (9 kernels) and one std cycle (4 kernels) --
+M times each.  Every per-cycle quantity (index list, Adam step, loss slot) is
+read from device counters, so the graphs are captured once and reused for
+every iteration.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib, specs
+from .buffer import ReplayBuffer
+from .device import DeviceNet, abi_dtype, device, torch_dtype
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class _Net:
+    """A trained network: parameters + Adam moments + step, all on device."""
+
+    def __init__(self, mlp, precision, lr, adam=None):
+        self.dn = DeviceNet(mlp, precision)
+        self.m = torch.zeros_like(self.dn.params)
+        self.v = torch.zeros_like(self.dn.params)
+        self.step = 0
+        self.lr = float(lr)
+        self.beta1, self.beta2, self.eps = 0.9, 0.999, 1e-8
+        if adam is not None:  # reference AdamState (nets.py:358-372)
+            self.m.copy_(torch.as_tensor(self.dn.pack(adam.m)))
+            self.v.copy_(torch.as_tensor(self.dn.pack(adam.v)))
+            self.step = int(adam.step)
+            self.lr, self.beta1, self.beta2, self.eps = adam.lr, adam.beta1, adam.beta2, adam.eps_adam
+        self.base = torch.zeros(1, device=self.m.device, dtype=torch.int64)
+
+
+class UpdateEngine:
+    """Device-resident M-cycle critic / actor / std-critic updates."""
+
+    def __init__(self, model, field, actor, critic, critic_target, std_net, buffer: ReplayBuffer, *,
+                 minibatch: int, k_s: float = 1.0, bootstrap: bool = True, tau: float = 0.005,
+                 lr_actor: float = 5e-4, lr_critic: float = 1e-3, lr_std: float = 1e-3,
+                 adam_states=None, precision: Optional[str] = None, use_graphs: bool = True,
+                 max_steps: int = 1 << 17):
+        self.model, self.field = model, field
+        self.precision = precision or buffer.precision
+        self.buffer = buffer
+        self.B = int(minibatch)
+        self.k_s, self.bootstrap, self.tau = float(k_s), bool(bootstrap), float(tau)
+        ad = adam_states or (None, None, None)
+        self.actor = _Net(actor, self.precision, lr_actor, ad[0])
+        self.critic = _Net(critic, self.precision, lr_critic, ad[1])
+        self.std = _Net(std_net, self.precision, lr_std, ad[2])
+        self.target = DeviceNet(critic_target, self.precision)
+        self.sysd = specs.system_struct(model)
+        self.costd = specs.cost_struct(model, field)
+        dev = device()
+        L = _lib.load()
+        B = self.B
+        self.ws_c = torch.empty(L.cacto_loss_workspace_bytes(self.critic.dn.desc, B), device=dev, dtype=torch.uint8)
+        self.ws_a = torch.empty(L.cacto_loss_workspace_bytes(self.actor.dn.desc, B), device=dev, dtype=torch.uint8)
+        self.ws_s = torch.empty(L.cacto_loss_workspace_bytes(self.std.dn.desc, B), device=dev, dtype=torch.uint8)
+        self.live = torch.zeros(1, device=dev, dtype=torch.int64)
+        self.cnt = torch.zeros(2, device=dev, dtype=torch.int64)   # [critic/actor cycle, std cycle]
+        # bias-correction tables bc[t] = 1 - beta**t in Python double precision (nets.py:380-381)
+        t = np.arange(max_steps + 2, dtype=np.float64)
+        self.bc = {}
+        for net in (self.actor, self.critic, self.std):
+            key = (net.beta1, net.beta2)
+            if key not in self.bc:
+                self.bc[key] = (torch.as_tensor(np.array([1.0 - net.beta1 ** k for k in t])).to(dev),
+                                torch.as_tensor(np.array([1.0 - net.beta2 ** k for k in t])).to(dev))
+        self.max_steps = max_steps
+        self.use_graphs = use_graphs
+        self._graphs = None
+        self._cap_M = 0
+        self.idx = None
+        self.closs = None
+        self.sloss = None
+        self.aloss = None
+
+    # -- one cycle, as kernel launches on the current stream -----------------------
+    def _batch(self, slot):
+        d = self.buffer.ring_desc(self.idx[slot], rows=self.B)
+        d.cycle = self.cnt[slot:slot + 1].data_ptr()
+        d.idx_stride = self.B
+        d.denom = 0
+        return d
+
+    def _adam(self, net: _Net, ws, npart, slot, target=None, loss=None):
+        bc1, bc2 = self.bc[(net.beta1, net.beta2)]
+        _lib.call("cacto_reduce_adam_graph", net.dn.desc.dtype, ws.data_ptr(), npart, net.dn.count,
+                  net.dn.params.data_ptr(), net.m.data_ptr(), net.v.data_ptr(), self.cnt[slot:slot + 1].data_ptr(),
+                  net.base.data_ptr(), bc1.data_ptr(), bc2.data_ptr(), net.lr, net.beta1, net.beta2, net.eps,
+                  None if target is None else target.params.data_ptr(), self.tau,
+                  None if loss is None else loss.data_ptr(), _stream())
+
+    def _cycle_critic_actor(self):
+        st = _stream()
+        bd = self._batch(0)
+        npart = ctypes.c_int32(0)
+        tgt = self.target if self.bootstrap else None
+        _lib.call("cacto_critic_loss", self.critic.dn.desc, tgt.desc if tgt else None, bd, self.k_s,
+                  int(self.bootstrap), self.ws_c.data_ptr(), self.ws_c.numel(), npart, st)
+        self._adam(self.critic, self.ws_c, npart.value, 0, target=self.target, loss=self.closs)  # trainer.py:216-220
+        _lib.call("cacto_count_live", bd, self.live.data_ptr(), st)
+        npa = ctypes.c_int32(0)
+        _lib.call("cacto_actor_loss", self.actor.dn.desc, self.critic.dn.desc, self.sysd, self.costd, bd,
+                  self.live.data_ptr(), self.ws_a.data_ptr(), self.ws_a.numel(), npa, st)
+        self._adam(self.actor, self.ws_a, npa.value, 0, loss=self.aloss)                        # trainer.py:223-225
+        _lib.call("cacto_counter_tick", self.cnt[0:1].data_ptr(), st)
+
+    def _cycle_std(self):
+        st = _stream()
+        bd = self._batch(1)
+        npart = ctypes.c_int32(0)
+        _lib.call("cacto_std_loss", self.std.dn.desc, self.critic.dn.desc, bd, self.ws_s.data_ptr(),
+                  self.ws_s.numel(), npart, st)
+        self._adam(self.std, self.ws_s, npart.value, 1, loss=self.sloss)                         # trainer.py:229-232
+        _lib.call("cacto_counter_tick", self.cnt[1:2].data_ptr(), st)
+
+    # -- buffers / graphs ---------------------------------------------------------------
+    def _alloc(self, M):
+        dev = device()
+        dt = torch_dtype(self.precision)
+        # index lists: [0] critic/actor cycles, [1] std cycles
+        self.idx = torch.zeros((2, M, self.B), device=dev, dtype=torch.int64)
+        self.closs = torch.zeros(M, device=dev, dtype=dt)
+        self.aloss = torch.zeros(M, device=dev, dtype=dt)
+        self.sloss = torch.zeros(M, device=dev, dtype=dt)
+        self._cap_M = M
+        self._graphs = None
+
+    def _capture(self):
+        """Capture one critic+actor cycle and one std cycle.  A first eager pass
+        (on snapshots) performs every lazy runtime set-up outside the capture."""
+        tensors = [self.actor.dn.params, self.actor.m, self.actor.v, self.critic.dn.params, self.critic.m,
+                   self.critic.v, self.std.dn.params, self.std.m, self.std.v, self.target.params, self.cnt]
+        saved = [t.clone() for t in tensors]
+        self.cnt.zero_()
+        self._cycle_critic_actor()
+        self._cycle_std()
+        torch.cuda.synchronize()
+        for t, s in zip(tensors, saved):
+            t.copy_(s)
+        g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g1, stream=side):
+                self._cycle_critic_actor()
+            with torch.cuda.graph(g2, stream=side):
+                self._cycle_std()
+        torch.cuda.current_stream().wait_stream(side)
+        self._graphs = (g1, g2)
+
+    # -- the update loop ----------------------------------------------------------------
+    def run(self, m_updates: int, rng: np.random.Generator):
+        """M critic+actor cycles then M std cycles (trainer.py:209-233).  Returns
+        (critic_losses [M], std_losses [M]) as float64 NumPy arrays."""
+        M = int(m_updates)
+        if M < 1:
+            raise ValueError("m_updates must be >= 1")
+        if self._cap_M < M:
+            self._alloc(M)
+        if self.critic.step + M >= self.max_steps:
+            raise ValueError("Adam step table exhausted; raise max_steps")
+        # the reference's minibatch stream: M lists for critic/actor, then M for std
+        lists = np.stack([self.buffer.draw_indices(self.B, rng) for _ in range(2 * M)])
+        stage = torch.zeros((2, self._cap_M, self.B), dtype=torch.int64)
+        stage[0, :M] = torch.as_tensor(lists[:M])
+        stage[1, :M] = torch.as_tensor(lists[M:])
+        self.idx.copy_(stage.pin_memory(), non_blocking=True)
+        for net in (self.actor, self.critic, self.std):
+            net.base.fill_(net.step)
+        if self.use_graphs and self._graphs is None:
+            self._capture()
+        self.cnt.zero_()
+        if self.use_graphs:
+            g1, g2 = self._graphs
+            for _ in range(M):
+                g1.replay()
+            for _ in range(M):
+                g2.replay()
+        else:
+            for _ in range(M):
+                self._cycle_critic_actor()
+            for _ in range(M):
+                self._cycle_std()
+        for net in (self.actor, self.critic, self.std):
+            net.step += M
+        closs = self.closs[:M].to("cpu", torch.float64).numpy()
+        sloss = self.sloss[:M].to("cpu", torch.float64).numpy()
+        return closs, sloss
+
+    # -- host views ------------------------------------------------------------------------
+    def networks(self):
+        """(actor, critic, critic_target, std) as reference-style networks."""
+        return (self.actor.dn.to_mlp(), self.critic.dn.to_mlp(), self.target.to_mlp(), self.std.dn.to_mlp())
+
+    def adam_host(self, net: _Net):
+        return net.dn.unpack(net.m), net.dn.unpack(net.v), net.step

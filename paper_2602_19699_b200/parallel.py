@@ -50,16 +50,18 @@ def gather_winners(scores: torch.Tensor, order: torch.Tensor, x0: torch.Tensor, 
     return torch.cat(all_s), torch.cat(all_o), torch.cat(all_x)
 
 
-def merge_positions(run_scores: torch.Tensor, keep: int, merge_fn: Callable):
+def merge_positions(run_scores: torch.Tensor, run_order: torch.Tensor, keep: int, merge_fn: Callable):
     """Positions (into the concatenated runs) of the global top-`keep`.
 
     Runs are contiguous shards in rank order and each run is sorted by
     (score desc, index asc), so ordering equal scores by run POSITION is the
     same as ordering them by global candidate index: the merge may carry
-    positions instead of indices (see cacto_select_merge).
+    positions instead of indices (see cacto_select_merge).  Padding rows
+    (run_order < 0) carry -1 and sort after every real candidate, NaN included.
     """
     R = run_scores.shape[0] // keep
     pos = torch.arange(R * keep, device=run_scores.device, dtype=torch.int64)
+    pos = torch.where(run_order < 0, torch.full_like(pos, -1), pos)
     return merge_fn(run_scores, pos, R, keep)
 
 
@@ -90,7 +92,7 @@ def sharded_select(local_scores: torch.Tensor, local_x0: torch.Tensor, base_inde
     order, top = local_topk(local_scores, k, base_index)
     x_sel = local_x0.index_select(0, order - base_index)
     rs, ro, rx = gather_winners(top, order, x_sel, keep, group)
-    pos = merge_positions(rs, keep, merge_fn)
+    pos = merge_positions(rs, ro, keep, merge_fn)
     return ro.index_select(0, pos), rx.index_select(0, pos)
 
 

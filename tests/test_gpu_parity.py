@@ -420,3 +420,80 @@ def test_bic_pipeline_vs_oracle_composition(mode, fp64):
     U = out["U"].cpu().numpy()
     _, U_ref, _, _ = O_nets.actor_rollout_batch(actor, spec, x0[got], 0, spec.t_max, None)
     assert rel(U, U_ref) < 1e-9
+
+
+# ---- device-resident update loop (trainer.py:208-234) ------------------------------
+
+def _oracle_update_loop(spec, fld, nets0, rows, B, M, seed, k_s=1.0, tau=0.005, lrs=(5e-4, 1e-3, 1e-3)):
+    from types import SimpleNamespace
+    from oracle import buffer as O_buffer
+    actor, critic, target, std = [list(n.flat_params()) for n in nets0]
+    mk = lambda tmpl, p: tmpl.with_params(p)  # noqa: E731
+    ring = O_buffer.Ring(spec.n, spec.m, 1 << 12)
+    ring.push_many(rows)
+    rng = np.random.default_rng(seed)
+    st = {k: ([np.zeros_like(p) for p in v], [np.zeros_like(p) for p in v], 0)
+          for k, v in (("a", actor), ("c", critic), ("s", std))}
+    closs, sloss = [], []
+    lists = [ring.draw_indices(B, rng) for _ in range(2 * M)]
+
+    def batch(idx):
+        g = ring.gather(idx)
+        return SimpleNamespace(t_max=spec.t_max, **g)
+
+    for i in range(M):
+        b = batch(lists[i])
+        l, g = O_nets.critic_loss(mk(nets0[1], critic), mk(nets0[2], target), b, k_s, True)
+        m_, v_, t_ = st["c"]
+        critic, m_, v_ = O_nets.adam_step(critic, m_, v_, g, t_, lrs[1])
+        st["c"] = (m_, v_, t_ + 1)
+        target = O_nets.polyak(target, critic, tau)
+        _, ga, _ = O_nets.actor_loss(mk(nets0[0], actor), mk(nets0[1], critic), spec, fld, b.xa)
+        m_, v_, t_ = st["a"]
+        actor, m_, v_ = O_nets.adam_step(actor, m_, v_, ga, t_, lrs[0])
+        st["a"] = (m_, v_, t_ + 1)
+        closs.append(l)
+    for i in range(M):
+        b = batch(lists[M + i])
+        l, g = O_nets.std_critic_loss(mk(nets0[3], std), mk(nets0[1], critic), b)
+        m_, v_, t_ = st["s"]
+        std, m_, v_ = O_nets.adam_step(std, m_, v_, g, t_, lrs[2])
+        st["s"] = (m_, v_, t_ + 1)
+        sloss.append(l)
+    return (actor, critic, target, std), np.array(closs), np.array(sloss)
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_update_engine_matches_oracle_loop(graphs, fp64):
+    from paper_2602_19699_b200.engine import UpdateEngine
+    spec, fld = B_specs.config("pointmass")
+    rng = np.random.default_rng(44)
+    c, h = B_specs.normalisation(spec)
+    d = spec.n + 1
+    actor = B_nets.init_mlp([d, 64, 64, 64, spec.m], rng, head="tanh", out_scale=spec.u_bound, in_center=c,
+                            in_half=h)
+    critic = B_nets.init_mlp([d, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+    target = B_nets.init_mlp([d, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+    std = B_nets.init_mlp([d, 64, 64, 64, 1], rng, head="std", in_center=c, in_half=h)
+    R = 700
+    lo, hi = O_envs.region_box(spec)
+    xa = np.concatenate([rng.uniform(size=(R, spec.n)) * (hi - lo) + lo, rng.integers(0, spec.t_max + 1, (R, 1))], 1)
+    xk = np.concatenate([rng.uniform(size=(R, spec.n)) * (hi - lo) + lo, rng.integers(1, spec.t_max + 1, (R, 1))], 1)
+    rows = {"xa": xa, "u": rng.normal(size=(R, spec.m)), "v_bar": rng.normal(size=R) * 10,
+            "v_bar_x": rng.normal(size=(R, spec.n)), "xa_plus_k": xk}
+    B, M = 48, 6
+    ref, ref_c, ref_s = _oracle_update_loop(spec, fld, (actor, critic, target, std), rows, B, M, seed=9)
+    buf = B_buffer.ReplayBuffer(spec.n, spec.m, spec.t_max, capacity=1 << 12)
+    buf.push_many(B_buffer.SampleBatch(rows["xa"], rows["u"], rows["v_bar"], rows["v_bar_x"], rows["xa_plus_k"],
+                                       spec.t_max))
+    eng = UpdateEngine(spec, fld, actor, critic, target, std, buf, minibatch=B, use_graphs=graphs)
+    closs, sloss = eng.run(M, np.random.default_rng(9))
+    np.testing.assert_allclose(closs, ref_c, rtol=1e-10)
+    np.testing.assert_allclose(sloss, ref_s, rtol=1e-10)
+    got = eng.networks()
+    for g_net, r_params in zip((got[0], got[1], got[2], got[3]), ref):
+        for a, b in zip(g_net.flat_params(), r_params):
+            np.testing.assert_allclose(a, b, rtol=1e-8, atol=1e-12)
+    # a second run continues the streams (Adam steps, buffer) like the reference's next iteration
+    closs2, _ = eng.run(M, np.random.default_rng(10))
+    assert np.all(np.isfinite(closs2))
