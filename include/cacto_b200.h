@@ -240,6 +240,9 @@ int cacto_sample_states(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, u
 /* -- measurement: FFMA/DFMA throughput kernel (roofline denominator of the
  * CUDA-core kernels); executes 2*16*8*iters*blocks*256 FLOPs. */
 int cacto_fma_peak(int32_t dtype, int32_t blocks, int32_t iters, void* out, void* stream);
+/* fp32 issue forms: 0 = FFMA with constant operands, 1 = 3-register FFMA (the GEMM
+ * inner-loop form), 2 = packed 3-register FFMA2 (fma.rn.f32x2); same FLOP count. */
+int cacto_fma_peak_mode(int32_t mode, int32_t blocks, int32_t iters, void* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,7 @@ SIGNATURES = {
     "cacto_counter_tick": (ctypes.c_int, [_P, _P]),
     "cacto_sample_states": (ctypes.c_int, [_U64, _U64, _U64, _U64, _I64, _I64, _I32, _P, _P, _P, _P]),
     "cacto_fma_peak": (ctypes.c_int, [_I32, _I32, _I32, _P, _P]),
+    "cacto_fma_peak_mode": (ctypes.c_int, [_I32, _I32, _I32, _P, _P]),
 }
 
 

@@ -120,11 +120,9 @@ CACTO_D void forward_output(const NS& net, const T* last, F f) {
   const int Lm = net.L - 1;
   const T* b = net.b(Lm);
   if (net.nh == 0)
-    TL::template narrow<IP>(last, net.out, [&](int j, int k) { return net.w(0, j, k); },
-                            [&](int s, int j, T v) { f(s, j, v + b[j]); });
+    TL::template narrow_rows<IP, NS::W0S>(last, net.W(0), net.out, [&](int s, int j, T v) { f(s, j, v + b[j]); });
   else
-    TL::template narrow<HP>(last, net.out, [&](int j, int k) { return net.w(Lm, j, k); },
-                            [&](int s, int j, T v) { f(s, j, v + b[j]); });
+    TL::template narrow_rows<HP, HP>(last, net.W(Lm), net.out, [&](int s, int j, T v) { f(s, j, v + b[j]); });
 }
 
 // Input-gradient sweep for output row j (nets.py:186-188 / 201-203):
@@ -165,8 +163,7 @@ CACTO_D void input_grad_sweep(const TL& tl, const NS& net, int act, int j, const
     gbuf = nb;
   }
   // s_0 = g_0 W_0  ([S][in], narrow over the input width)
-  TL::template narrow<HP>(gbuf, net.in, [&](int c, int k) { return net.w(0, k, c); },
-                          [&](int s, int c, T v) { f(s, c, v); });
+  TL::template narrow_cols<HP, NS::W0S, NS::kIP>(gbuf, net.W(0), net.in, [&](int s, int c, T v) { f(s, c, v); });
   __syncthreads();
 }
 

@@ -8,6 +8,8 @@
 //   dynamics    x_s <- f(x_s, u_s), stage cost l(x_s, u_s) accumulated in the
 //               thread that owns start s, in NumPy's pairwise-sum order, so
 //               cost == Trajectory.cost (ilqr.py:76-78) term for term.
+#include <stdlib.h>
+
 #include "net.cuh"
 #include "systems.cuh"
 
@@ -202,10 +204,22 @@ static int launch_rollout_s(const RolloutArgs<T>& a, cudaStream_t st) {
 // Tile size: 128 starts per CTA (2 CTAs / SM) when the batch fills the GPU,
 // 32-start tiles for small batches (e.g. the kept warm-start re-rollout) so
 // that the CTAs still cover every SM.
+static int tile_override() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CACTO_ROLLOUT_TILE");  // 128 / 256 (experiments)
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <typename T, int SYS, int HP>
 static int launch_rollout(const RolloutArgs<T>& a, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
-    if (a.N >= (int64_t)256 * num_sms() && HP == 64) return launch_rollout_s<T, SYS, HP, 256>(a, st);
+    // 128-start tiles (2 CTAs / SM, 4x8 micro-tiles) measured faster than 256-start
+    // tiles (1 CTA / SM, 8x8) on B200: 4.13 vs 4.57 ms (profiles/README.md)
+    const int ov = tile_override();
+    if (ov == 256 && a.N >= (int64_t)256 * num_sms() && HP == 64) return launch_rollout_s<T, SYS, HP, 256>(a, st);
     if (a.N >= (int64_t)128 * num_sms()) return launch_rollout_s<T, SYS, HP, 128>(a, st);
     return launch_rollout_s<T, SYS, HP, 32>(a, st);
   } else {

@@ -171,26 +171,101 @@ struct Tile {
     }
   }
 
-  // narrow output: for every (s, j<nout): f(s, j, sum_{k<K} A[k][s] * w(j, k))
-  // 4 lanes split K and combine with shuffles (K % 4 == 0).
-  template <int K, typename WF, typename F>
-  CACTO_D static void narrow(const T* __restrict__ A, int nout, WF w, F f) {
-    const int total = S * nout * 4;
-    for (int base = 0; base < total; base += kThreads) {
-      int idx = base + threadIdx.x;
-      bool live = idx < total;
-      int q = idx & 3, p = idx >> 2;
-      int s = p % S, j = p / S;
-      T sum = T(0);
-      if (live) {
-        const uint32_t ab = saddr(A);
-#pragma unroll 4
-        for (int k = q * (K / 4); k < (q + 1) * (K / 4); ++k)
-          sum = fma(lds1(ab + (uint32_t)at(k, s) * (uint32_t)sizeof(T), (T*)nullptr), w(j, k), sum);
+  // narrow output (nout <= 8 columns): f(s, j, sum_{k<K} A[k][s] * W[j][k]),
+  // W rows of stride WC (swizzled with KS).  Work item = (sample, K-quarter);
+  // the 4 quarter lanes of a sample are adjacent and combine with shuffles.
+  // Per 4 rows: 4 scalar A loads (one row key per 4-row group when TN >= 4),
+  // one 16-byte W load per output, 4*nout FMAs.
+  template <int K, int WC, typename F>
+  CACTO_D static void narrow_rows(const T* __restrict__ A, const T* __restrict__ W, int nout, F f) {
+    static_assert(K % 16 == 0 || K == 8, "K must split into 4-row groups per quarter");
+    constexpr int Q = (K >= 16) ? 4 : 2;
+    constexpr int KQ = K / Q;
+    constexpr int KMW = (WC / 4 >= 8 ? 8 : WC / 4) - 1;
+    constexpr uint32_t ES = sizeof(T);
+    const uint32_t abase = saddr(A), wbase = saddr(W);
+    for (int item = threadIdx.x; item < S * Q; item += kThreads) {
+      const int s = item / Q, q = item % Q;
+      const int sc = s >> 2, s3 = s & 3;
+      T acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = T(0);
+      const uint32_t ab = abase + (uint32_t)(q * KQ * S + s3) * ES;
+#pragma unroll
+      for (int kk = 0; kk < KQ; kk += 4) {
+        const int k0 = q * KQ + kk;
+        T a[4];
+        if constexpr (KS >= 2) {
+          const uint32_t off = (uint32_t)((sc ^ ((k0 >> KS) & KMS)) << 2) * ES;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) a[r] = lds1(ab + (uint32_t)((kk + r) * S) * ES + off, (T*)nullptr);
+        } else {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            a[r] = lds1(ab + (uint32_t)((kk + r) * S + ((sc ^ (((k0 + r) >> KS) & KMS)) << 2)) * ES, (T*)nullptr);
+        }
+        const int kc = k0 >> 2;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < nout) {
+            V4<T> w = lds4(wbase + (uint32_t)(j * WC + ((kc ^ ((j >> KS) & KMW)) << 2)) * ES, (T*)nullptr);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[j] = fma(a[r], w.v[r], acc[j]);
+          }
+        }
       }
-      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-      if (live && q == 0) f(s, j, sum);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < nout) {
+          T v = acc[j];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          if constexpr (Q == 4) v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (q == 0) f(s, j, v);
+        }
+      }
+    }
+  }
+
+  // transposed narrow (nout <= NMAX columns): f(s, c, sum_{k<K} A[k][s] * W[k][c]),
+  // W [K][WC] rows swizzled with KS -- the input-gradient s_0 = g_0 W_0.
+  template <int K, int WC, int NMAX, typename F>
+  CACTO_D static void narrow_cols(const T* __restrict__ A, const T* __restrict__ W, int nout, F f) {
+    static_assert(NMAX % 4 == 0 && NMAX <= WC, "column block");
+    static_assert(K % 16 == 0, "K must split into 4 quarters of 4-row groups");
+    constexpr int Q = 4, KQ = K / Q;
+    constexpr int KMW = (WC / 4 >= 8 ? 8 : WC / 4) - 1;
+    constexpr uint32_t ES = sizeof(T);
+    const uint32_t abase = saddr(A), wbase = saddr(W);
+    for (int item = threadIdx.x; item < S * Q; item += kThreads) {
+      const int s = item / Q, q = item % Q;
+      const int sc = s >> 2, s3 = s & 3;
+      T acc[NMAX];
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c) acc[c] = T(0);
+      const uint32_t ab = abase + (uint32_t)(q * KQ * S + s3) * ES;
+#pragma unroll 4
+      for (int kk = 0; kk < KQ; ++kk) {
+        const int k = q * KQ + kk;
+        const T a = lds1(ab + (uint32_t)(kk * S + ((sc ^ ((k >> KS) & KMS)) << 2)) * ES, (T*)nullptr);
+        const int wk = (k >> KS) & KMW;
+#pragma unroll
+        for (int cc = 0; cc < NMAX / 4; ++cc) {
+          if (4 * cc < nout) {
+            V4<T> w = lds4(wbase + (uint32_t)(k * WC + ((cc ^ wk) << 2)) * ES, (T*)nullptr);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[4 * cc + e] = fma(a, w.v[e], acc[4 * cc + e]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c) {
+        if (c < nout) {
+          T v = acc[c];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (q == 0) f(s, c, v);
+        }
+      }
     }
   }
 
