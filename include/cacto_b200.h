@@ -237,6 +237,14 @@ int cacto_sample_states(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, u
                         int64_t first_row, int64_t N, int32_t n, const double* lo, const double* hi,
                         double* x, void* stream);
 
+/* -- tcgen05 tensor-core GEMM for the wide layers (H >= 128):
+ * D[m][n] (+)= alpha * sum_k A(m,k) B(n,k), A(m,k) = A[m*sam + k*sak],
+ * B(n,k) = B[n*sbn + k*sbk], D row-major with leading dimension ldd, fp32.
+ * passes = 3: 3xTF32 split (fp32-faithful); passes = 1: plain TF32. */
+int cacto_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, int64_t sam, int64_t sak, const float* B,
+                    int64_t sbn, int64_t sbk, float* D, int64_t ldd, int32_t accumulate, float alpha,
+                    int32_t passes, void* stream);
+
 /* -- measurement: FFMA/DFMA throughput kernel (roofline denominator of the
  * CUDA-core kernels); executes 2*16*8*iters*blocks*256 FLOPs. */
 int cacto_fma_peak(int32_t dtype, int32_t blocks, int32_t iters, void* out, void* stream);
