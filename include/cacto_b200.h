@@ -239,11 +239,14 @@ int cacto_sample_states(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, u
 
 /* -- tcgen05 tensor-core GEMM for the wide layers (H >= 128):
  * D[m][n] (+)= alpha * sum_k A(m,k) B(n,k), A(m,k) = A[m*sam + k*sak],
- * B(n,k) = B[n*sbn + k*sbk], D row-major with leading dimension ldd, fp32.
- * passes = 3: 3xTF32 split (fp32-faithful); passes = 1: plain TF32. */
+ * B(n,k) = B[n*sbn + k*sbk] (each operand K-major or MN-major, 16-byte aligned
+ * rows), D row-major with leading dimension ldd, fp32.  passes = 3: 3xTF32 split
+ * (fp32-faithful); passes = 1: plain TF32.  Long-K shapes that cannot fill the GPU
+ * use split-K partials in `workspace` (cacto_gemm_workspace_bytes; deterministic). */
+size_t cacto_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
 int cacto_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, int64_t sam, int64_t sak, const float* B,
                     int64_t sbn, int64_t sbk, float* D, int64_t ldd, int32_t accumulate, float alpha,
-                    int32_t passes, void* stream);
+                    int32_t passes, void* workspace, size_t workspace_bytes, void* stream);
 
 /* -- measurement: FFMA/DFMA throughput kernel (roofline denominator of the
  * CUDA-core kernels); executes 2*16*8*iters*blocks*256 FLOPs. */

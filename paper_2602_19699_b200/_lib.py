@@ -101,8 +101,9 @@ SIGNATURES = {
                                                 _D, _P, _D, _P, _P]),
     "cacto_counter_tick": (ctypes.c_int, [_P, _P]),
     "cacto_sample_states": (ctypes.c_int, [_U64, _U64, _U64, _U64, _I64, _I64, _I32, _P, _P, _P, _P]),
+    "cacto_gemm_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
     "cacto_gemm_tf32": (ctypes.c_int, [_I32, _I32, _I32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I32,
-                                        ctypes.c_float, _I32, _P]),
+                                        ctypes.c_float, _I32, _P, _SZ, _P]),
     "cacto_fma_peak": (ctypes.c_int, [_I32, _I32, _I32, _P, _P]),
     "cacto_fma_peak_mode": (ctypes.c_int, [_I32, _I32, _I32, _P, _P]),
 }

@@ -2,21 +2,29 @@
 // (H = 128..512, north_star: "tensor-core tcgen05 GEMMs only for the wide
 // batched layers").
 //
-//   D[m][n] (+)= sum_k A(m, k) * B(n, k)       fp32 in / fp32 out
+//   D[m][n] (+)= alpha * sum_k A(m, k) * B(n, k)       fp32 in / fp32 out
 //
-// A(m,k) = A[m*sam + k*sak], B(n,k) = B[n*sbn + k*sbk]: any of the three GEMMs of a
-// dense layer (z = a W^T, s = g W, gW = g^T a) is one call with the right strides.
-// fp32 accuracy with TF32 tensor cores: every operand is split x = hi + lo
-// (hi = tf32(x), lo = tf32(x - hi)) and D accumulates hi*hi + hi*lo + lo*hi
-// ("3xTF32"; relative error ~1e-6, vs ~1e-3 for a single TF32 pass).
+// A(m,k) = A[m*sam + k*sak], B(n,k) = B[n*sbn + k*sbk]; each operand is either
+// K-major (sak == 1) or MN-major (sam == 1), so the three GEMMs of a dense layer
+// (z = a W^T, s = g W, gW = g^T a) are plain calls with no transposes.
 //
-// CTA = one 128 x BN output tile (UMMA M = 128, cta_group::1, N = BN <= 256).
-//   warps 0-3  producers: global fp32 -> split -> canonical K-major SWIZZLE_128B
-//              smem tiles (32 fp32 = 128 B per row, chunk ^= row % 8), 2 stages;
-//              then the epilogue: tcgen05.ld 32x32b -> registers -> global
-//   warp 4     one elected lane issues tcgen05.mma.kind::tf32 (4 K-steps of 8 per
-//              128-byte row, x3 products) and commits to the stage's mbarrier
-// The accumulator lives in TMEM (128 lanes x BN fp32 columns).
+// fp32 accuracy from TF32 tensor cores ("3xTF32"): the tensor core reads a raw
+// fp32 operand as its TF32 truncation hi = trunc(x); split warps compute
+// lo = x - hi in shared memory and the MMA issues hi*hi + hi*lo + lo*hi.
+//
+// Pipeline (one 128 x BN output tile per CTA, 3 shared-memory stages):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2D loads straight into the
+//               canonical UMMA layouts (K-major: 128B swizzle; MN-major: 128B
+//               swizzle with 32-byte atoms, the tf32 MN-major layout), one
+//               mbarrier per stage
+//   warps 1-4   split workers (lo tiles, layout-agnostic smem->smem), then the
+//               epilogue: tcgen05.ld 32x32b -> registers -> global
+//   warp 5      one elected lane issues tcgen05.mma.cta_group::1.kind::tf32
+//               (M = 128, N = BN, K = 8 per instruction) and commits to the
+//               stage's "empty" mbarrier; TMEM holds the 128 x BN accumulator
+// Split-K over grid.z writes per-split partials (deterministic reduce after).
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace cacto {
@@ -24,15 +32,18 @@ namespace cacto {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;  // fp32 elements per 128-byte row
-constexpr int kProducers = 128;
-constexpr int kThreadsTC = 160;
+constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int kStages = 3;
+constexpr int kThreadsTC = 192;
 
 CACTO_D void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
 }
 CACTO_D void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+CACTO_D void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %0;" ::"r"(bytes), "r"(saddr(bar)) : "memory");
 }
 CACTO_D void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -52,28 +63,30 @@ CACTO_D void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
                : "memory");
 }
-CACTO_D uint32_t tf32_round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
+CACTO_D void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          saddr(dst)),
+      "l"((uint64_t)map), "r"(saddr(bar)), "r"(c0), "r"(c1)
+      : "memory");
 }
 
-// SWIZZLE_128B K-major smem descriptor (version 1 = Blackwell): start address,
-// SBO = 1024 B between 8-row groups, LBO unused for swizzled K-major.
-CACTO_D uint64_t make_desc(uint32_t saddr_bytes) {
+// smem matrix descriptor (version 1 = Blackwell); layout 2 = SWIZZLE_128B,
+// 1 = SWIZZLE_128B_BASE32B (the only MN-major layout tcgen05 accepts for tf32)
+CACTO_D uint64_t make_desc(uint32_t saddr_bytes, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr_bytes >> 4) & 0x3FFF);
-  d |= (uint64_t)(1) << 16;                 // LBO (ignored)
-  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;  // SBO
-  d |= (uint64_t)1 << 46;                   // version
-  d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
-// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = BN
-template <int BN>
-constexpr uint32_t idesc_tf32() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor: D f32, A/B tf32, M = 128, N = BN, majorness per operand
+CACTO_HD uint32_t idesc_tf32(int bn, int a_mn_major, int b_mn_major) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn_major << 15) | ((uint32_t)b_mn_major << 16) |
+         ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 CACTO_D void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
@@ -85,150 +98,51 @@ CACTO_D void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
       : "memory");
 }
 
-// byte offset of element (row, k) of a [rows][32] fp32 tile in the SW128 layout
-CACTO_D uint32_t sw128(int row, int k) {
-  return (uint32_t)(row * 128 + ((((k >> 2) ^ (row & 7))) << 4) + ((k & 3) << 2));
-}
-
 struct GemmArgs {
   int M, N, K;
-  const float* A;
-  int64_t sam, sak;
-  const float* B;
-  int64_t sbn, sbk;
+  int a_kmajor, b_kmajor;
+  int passes;
   float* D;
   int64_t ldd;
-  int accumulate;  // D += product (else D = product)
+  int accumulate;
   float alpha;
+  int kb_per_split;
+  int64_t split_stride;  // elements between per-split partial outputs (0: no split)
 };
 
-// producers: fill stage buffers for k-block kb (hi and lo parts of A and B tiles)
-template <int BN>
-CACTO_D void produce(const GemmArgs& g, int m0, int n0, int kb, unsigned char* sA_hi, unsigned char* sA_lo,
-                     unsigned char* sB_hi, unsigned char* sB_lo) {
-  const int t = threadIdx.x;  // 0..127
-  const int k0 = kb * BK;
-  // A tile [BM][BK]
-  if (g.sak == 1) {
-    for (int e = t * 4; e < BM * BK; e += kProducers * 4) {
-      const int r = e / BK, c = e % BK;
-      const int m = m0 + r, k = k0 + c;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < g.M) {
-        const float* p = g.A + (int64_t)m * g.sam + k;
-        if (k + 3 < g.K && (((uintptr_t)p) & 15) == 0) {
-          v = *reinterpret_cast<const float4*>(p);
-        } else {
-          v.x = k < g.K ? p[0] : 0.f;
-          v.y = k + 1 < g.K ? p[1] : 0.f;
-          v.z = k + 2 < g.K ? p[2] : 0.f;
-          v.w = k + 3 < g.K ? p[3] : 0.f;
-        }
-      }
-      const float x[4] = {v.x, v.y, v.z, v.w};
-      uint32_t hi[4], lo[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        hi[q] = tf32_round(x[q]);
-        lo[q] = tf32_round(x[q] - __uint_as_float(hi[q]));
-      }
-      const uint32_t off = sw128(r, c);
-      *reinterpret_cast<uint4*>(sA_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(sA_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    }
-  } else {  // M-contiguous: lanes walk m (coalesced), each thread one row, 32 k values
-    for (int r = t; r < BM; r += kProducers) {
-      const int m = m0 + r;
-      for (int c = 0; c < BK; c += 4) {
-        float x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int k = k0 + c + q;
-          x[q] = (m < g.M && k < g.K) ? g.A[(int64_t)m * g.sam + (int64_t)k * g.sak] : 0.f;
-        }
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          hi[q] = tf32_round(x[q]);
-          lo[q] = tf32_round(x[q] - __uint_as_float(hi[q]));
-        }
-        const uint32_t off = sw128(r, c);
-        *reinterpret_cast<uint4*>(sA_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(sA_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
-    }
-  }
-  // B tile [BN][BK]
-  if (g.sbk == 1) {
-    for (int e = t * 4; e < BN * BK; e += kProducers * 4) {
-      const int r = e / BK, c = e % BK;
-      const int n = n0 + r, k = k0 + c;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (n < g.N) {
-        const float* p = g.B + (int64_t)n * g.sbn + k;
-        if (k + 3 < g.K && (((uintptr_t)p) & 15) == 0) {
-          v = *reinterpret_cast<const float4*>(p);
-        } else {
-          v.x = k < g.K ? p[0] : 0.f;
-          v.y = k + 1 < g.K ? p[1] : 0.f;
-          v.z = k + 2 < g.K ? p[2] : 0.f;
-          v.w = k + 3 < g.K ? p[3] : 0.f;
-        }
-      }
-      const float x[4] = {v.x, v.y, v.z, v.w};
-      uint32_t hi[4], lo[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        hi[q] = tf32_round(x[q]);
-        lo[q] = tf32_round(x[q] - __uint_as_float(hi[q]));
-      }
-      const uint32_t off = sw128(r, c);
-      *reinterpret_cast<uint4*>(sB_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(sB_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    }
-  } else {
-    for (int r = t; r < BN; r += kProducers) {
-      const int n = n0 + r;
-      for (int c = 0; c < BK; c += 4) {
-        float x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int k = k0 + c + q;
-          x[q] = (n < g.N && k < g.K) ? g.B[(int64_t)n * g.sbn + (int64_t)k * g.sbk] : 0.f;
-        }
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          hi[q] = tf32_round(x[q]);
-          lo[q] = tf32_round(x[q] - __uint_as_float(hi[q]));
-        }
-        const uint32_t off = sw128(r, c);
-        *reinterpret_cast<uint4*>(sB_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(sB_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
-    }
-  }
+// descriptors of the k-step `kk` (8 tf32) of an operand tile
+//  K-major : SW128 atoms of 8 rows x 128 B; a k-step is 32 B inside the row
+//  MN-major: SW128_BASE32B atoms of 4 k-rows x 128 B (32 MN elements, SBO = 512 B),
+//            MN blocks of 32 at LBO = 4 KB (one TMA box each); a k-step = 8 rows
+CACTO_D uint64_t op_desc(uint32_t tile, int kmajor, int kk) {
+  if (kmajor) return make_desc(tile + kk * 32, 16, 1024, 2);
+  return make_desc(tile + kk * 1024, 4096, 512, 1);
 }
 
-template <int BN, int PASSES>
-__global__ void __launch_bounds__(kThreadsTC, 1) gemm_tf32_kernel(const GemmArgs g) {
-  constexpr int STAGES = 2;
+template <int BN>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmArgs g) {
   constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
-  constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // raw A, raw B, lo A, lo B
   constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
-  // 1024-byte alignment of the swizzle atoms
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], done_bar;
+  __shared__ __align__(8) uint64_t tma_bar[kStages], split_bar[kStages], empty_bar[kStages], done_bar;
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int nkb = (g.K + BK - 1) / BK;
+  const int nkb_all = (g.K + BK - 1) / BK;
+  const int kb0 = blockIdx.z * g.kb_per_split;
+  const int kb1 = min(nkb_all, kb0 + g.kb_per_split);
+  const int nkb = kb1 - kb0;
+  const bool three = g.passes == 3;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], kProducers);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&tma_bar[s], 1);
+      mbar_init(&split_bar[s], 128);
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&done_bar, 1);
@@ -245,66 +159,123 @@ __global__ void __launch_bounds__(kThreadsTC, 1) gemm_tf32_kernel(const GemmArgs
   tc_fence_after();
   const uint32_t tmem_d = tmem_base_sh;
 
-  if (warp < 4) {
-    // ---- producers -----------------------------------------------------------
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&empty_bar[s], ph ^ 1);
-      unsigned char* st = base + s * STAGE_BYTES;
-      produce<BN>(g, m0, n0, kb, st, st + A_BYTES, st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES);
-      fence_async_smem();
-      mbar_arrive(&full_bar[s]);
+  if (warp == 0) {
+    // ---- TMA producer -------------------------------------------------------------
+    if (lane == 0 && nkb > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (i / kStages) & 1;
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        unsigned char* st = base + s * STAGE_BYTES;
+        const int k0 = (kb0 + i) * BK;
+        mbar_expect_tx(&tma_bar[s], A_BYTES + B_BYTES);
+        if (g.a_kmajor) {
+          tma_load_2d(st, &tmA, &tma_bar[s], k0, m0);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &tmA, &tma_bar[s], m0 + 32 * j, k0);
+        }
+        if (g.b_kmajor) {
+          tma_load_2d(st + A_BYTES, &tmB, &tma_bar[s], k0, n0);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j) tma_load_2d(st + A_BYTES + j * 4096, &tmB, &tma_bar[s], n0 + 32 * j, k0);
+        }
+      }
     }
-    // ---- epilogue: TMEM -> registers -> global -----------------------------------
-    mbar_wait(&done_bar, 0);
-    tc_fence_after();
-    const int row = m0 + warp * 32 + lane;
+  } else if (warp <= 4) {
+    // ---- split workers: lo = x - trunc_tf32(x) (layout-agnostic) -----------------
+    const int t = threadIdx.x - 32;  // 0..127
+    if (three) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (i / kStages) & 1;
+        mbar_wait(&tma_bar[s], ph);
+        unsigned char* st = base + s * STAGE_BYTES;
+        const float4* src = reinterpret_cast<const float4*>(st);
+        float4* dst = reinterpret_cast<float4*>(st + A_BYTES + B_BYTES);
+        constexpr int NV = (A_BYTES + B_BYTES) / 16;
+#pragma unroll 4
+        for (int q = t; q < NV; q += 128) {
+          float4 x = src[q];
+          float4 lo;
+          lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          dst[q] = lo;
+        }
+        fence_async_smem();
+        mbar_arrive(&split_bar[s]);
+      }
+    }
+    // ---- epilogue: TMEM -> registers -> global --------------------------------------
+    const int lane_grp = warp & 3;  // tcgen05.ld lane quarter of this warp
+    const int row = m0 + lane_grp * 32 + lane;
+    float* dbase = g.D + (int64_t)blockIdx.z * g.split_stride;
+    if (nkb > 0) {
+      mbar_wait(&done_bar, 0);
+      tc_fence_after();
+    }
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
       uint32_t v[16];
-      const uint32_t taddr = tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-          "%14, %15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < g.M) {
-        float* d = g.D + (int64_t)row * g.ldd + n0 + c0;
+      if (nkb > 0) {
+        const uint32_t taddr = tmem_d + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          if (n0 + c0 + q < g.N) {
-            float val = g.alpha * __uint_as_float(v[q]);
-            d[q] = g.accumulate ? d[q] + val : val;
+        for (int q = 0; q < 16; ++q) v[q] = 0u;
+      }
+      if (row < g.M) {
+        float* d = dbase + (int64_t)row * g.ldd + n0 + c0;
+        if (n0 + c0 + 16 <= g.N && !g.accumulate && ((((uintptr_t)d) & 15) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 16; q += 4)
+            *reinterpret_cast<float4*>(d + q) =
+                make_float4(g.alpha * __uint_as_float(v[q]), g.alpha * __uint_as_float(v[q + 1]),
+                            g.alpha * __uint_as_float(v[q + 2]), g.alpha * __uint_as_float(v[q + 3]));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (n0 + c0 + q < g.N) {
+              float val = g.alpha * __uint_as_float(v[q]);
+              d[q] = g.accumulate ? d[q] + val : val;
+            }
           }
         }
       }
     }
-  } else if (warp == 4) {
-    // ---- MMA issuer (one lane) --------------------------------------------------
-    constexpr uint32_t idesc = idesc_tf32<BN>();
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&full_bar[s], ph);
+  } else {
+    // ---- MMA issuer ---------------------------------------------------------------------
+    const uint32_t idesc = idesc_tf32(BN, !g.a_kmajor, !g.b_kmajor);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kStages;
+      const uint32_t ph = (i / kStages) & 1;
+      mbar_wait(three ? &split_bar[s] : &tma_bar[s], ph);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t st = saddr(base + s * STAGE_BYTES);
-        const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+        const uint32_t a_raw = st, b_raw = st + A_BYTES, a_lo = st + A_BYTES + B_BYTES, b_lo = a_lo + A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {  // UMMA_K = 8 tf32 = 32 bytes
-          const uint32_t ko = kk * 32;
-          const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem_d, make_desc(a_hi + ko), make_desc(b_hi + ko), idesc, acc0);
-          if (PASSES == 3) {
-            mma_tf32(tmem_d, make_desc(a_hi + ko), make_desc(b_lo + ko), idesc, 1u);
-            mma_tf32(tmem_d, make_desc(a_lo + ko), make_desc(b_hi + ko), idesc, 1u);
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
+          mma_tf32(tmem_d, op_desc(a_raw, g.a_kmajor, kk), op_desc(b_raw, g.b_kmajor, kk), idesc, acc0);
+          if (three) {
+            mma_tf32(tmem_d, op_desc(a_raw, g.a_kmajor, kk), op_desc(b_lo, g.b_kmajor, kk), idesc, 1u);
+            mma_tf32(tmem_d, op_desc(a_lo, g.a_kmajor, kk), op_desc(b_raw, g.b_kmajor, kk), idesc, 1u);
           }
         }
         tc_commit(&empty_bar[s]);
-        if (kb == nkb - 1) tc_commit(&done_bar);
+        if (i == nkb - 1) tc_commit(&done_bar);
       }
       __syncwarp();
     }
@@ -316,39 +287,145 @@ __global__ void __launch_bounds__(kThreadsTC, 1) gemm_tf32_kernel(const GemmArgs
   }
 }
 
-template <int BN, int PASSES>
-static int launch_gemm(const GemmArgs& g, cudaStream_t st) {
+// ---- host: tensor maps ------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// operand with element (r, k) at X[r*sr + k*sk], rows x K; box_rows for K-major
+static int make_map(CUtensorMap* map, const float* X, int rows, int K, int64_t sr, int64_t sk, int box_rows,
+                    int* kmajor) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return set_error(CACTO_ECUDA, "gemm: cuTensorMapEncodeTiled unavailable");
+  if (((uintptr_t)X) & 15) return set_error(CACTO_EVALUE, "gemm: operand not 16-byte aligned");
+  cuuint64_t dims[2], strides[1];
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (sk == 1) {
+    *kmajor = 1;
+    dims[0] = (cuuint64_t)K;
+    dims[1] = (cuuint64_t)rows;
+    strides[0] = (cuuint64_t)sr * 4;
+    box[0] = BK;
+    box[1] = (cuuint32_t)box_rows;
+  } else if (sr == 1) {
+    *kmajor = 0;
+    dims[0] = (cuuint64_t)rows;
+    dims[1] = (cuuint64_t)K;
+    strides[0] = (cuuint64_t)sk * 4;
+    box[0] = 32;
+    box[1] = BK;
+  } else {
+    return set_error(CACTO_EVALUE, "gemm: operands must be K-major or MN-major");
+  }
+  if (strides[0] % 16) return set_error(CACTO_EVALUE, "gemm: operand row stride must be a multiple of 16 bytes");
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)X, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   *kmajor ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(CACTO_ECUDA, "gemm: tensor map encode failed (%d)", (int)r);
+  return CACTO_OK;
+}
+
+template <int BN>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& g, int splits,
+                       cudaStream_t st) {
   constexpr uint32_t STAGE_BYTES = 2 * BM * BK * 4 + 2 * BN * BK * 4;
-  const size_t smem = 2 * STAGE_BYTES + 1024;
-  auto kern = gemm_tf32_kernel<BN, PASSES>;
+  const size_t smem = kStages * STAGE_BYTES + 1024;
+  auto kern = gemm_tf32_kernel<BN>;
   if (!ensure_smem((const void*)kern, smem)) return set_error(CACTO_ECUDA, "gemm: %zu B smem unavailable", smem);
-  dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN);
-  kern<<<grid, kThreadsTC, smem, st>>>(g);
+  dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, splits);
+  kern<<<grid, kThreadsTC, smem, st>>>(ma, mb, g);
   return check_launch("gemm_tf32_kernel");
+}
+
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int M, int N,
+                                     int64_t ldp, float* D, int64_t ldd, int accumulate) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / N, n = e - m * N;
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[z * split_stride + m * ldp + n];
+    float* d = D + m * ldd + n;
+    *d = accumulate ? *d + s : s;
+  }
 }
 
 }  // namespace tc
 
-int gemm_tf32(const tc::GemmArgs& g, int passes, cudaStream_t st) {
-  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return CACTO_OK;
-  // N tile: 128 (TMEM 128 columns) unless the problem is narrow
-  if (passes == 3) {
-    if (g.N <= 64) return tc::launch_gemm<64, 3>(g, st);
-    return tc::launch_gemm<128, 3>(g, st);
+// workspace bytes a gemm of this shape may need for split-K partials
+size_t gemm_workspace_bytes(int M, int N, int K) {
+  const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + 127) / 128);
+  const int nkb = (K + tc::BK - 1) / tc::BK;
+  int splits = 1;
+  while (tiles * splits * 2 <= num_sms() && nkb / (splits * 2) >= 8) splits *= 2;
+  return splits > 1 ? (size_t)splits * M * N * 4 : 0;
+}
+
+int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk,
+              float* D, int64_t ldd, int accumulate, float alpha, int passes, void* ws, size_t ws_bytes,
+              cudaStream_t st) {
+  if (M <= 0 || N <= 0) return CACTO_OK;
+  const int bn = N <= 64 ? 64 : 128;
+  CUtensorMap ma, mb;
+  tc::GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.passes = passes;
+  int rc = tc::make_map(&ma, A, M, K, sam, sak, tc::BM, &g.a_kmajor);
+  if (rc) return rc;
+  rc = tc::make_map(&mb, B, N, K, sbn, sbk, bn, &g.b_kmajor);
+  if (rc) return rc;
+  // split-K when the tile grid cannot fill the GPU and K is long (weight gradients)
+  const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + bn - 1) / bn);
+  const int nkb = (K + tc::BK - 1) / tc::BK;
+  int splits = 1;
+  while (tiles * splits * 2 <= num_sms() && nkb / (splits * 2) >= 8) splits *= 2;
+  if (splits > 1 && (!ws || ws_bytes < (size_t)splits * M * N * 4)) splits = 1;
+  g.kb_per_split = (nkb + splits - 1) / splits;
+  g.alpha = alpha;
+  if (splits > 1) {
+    g.D = (float*)ws;
+    g.ldd = N;
+    g.accumulate = 0;
+    g.split_stride = (int64_t)M * N;
+  } else {
+    g.D = D;
+    g.ldd = ldd;
+    g.accumulate = accumulate;
+    g.split_stride = 0;
   }
-  if (g.N <= 64) return tc::launch_gemm<64, 1>(g, st);
-  return tc::launch_gemm<128, 1>(g, st);
+  rc = bn == 64 ? tc::launch_gemm<64>(ma, mb, g, splits, st) : tc::launch_gemm<128>(ma, mb, g, splits, st);
+  if (rc || splits == 1) return rc;
+  int64_t total = (int64_t)M * N;
+  unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 8 * num_sms());
+  tc::splitk_reduce_kernel<<<grid, 256, 0, st>>>((const float*)ws, splits, (int64_t)M * N, M, N, N, D, ldd, accumulate);
+  return check_launch("splitk_reduce_kernel");
 }
 
 }  // namespace cacto
 
 using namespace cacto;
 
+extern "C" size_t cacto_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) { return gemm_workspace_bytes(M, N, K); }
+
 extern "C" int cacto_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, int64_t sam, int64_t sak,
                                const float* B, int64_t sbn, int64_t sbk, float* D, int64_t ldd, int32_t accumulate,
-                               float alpha, int32_t passes, void* stream) {
+                               float alpha, int32_t passes, void* workspace, size_t workspace_bytes, void* stream) {
   if (!A || !B || !D || M < 0 || N < 0 || K < 0) return set_error(CACTO_EVALUE, "gemm: bad arguments");
   if (passes != 1 && passes != 3) return set_error(CACTO_EVALUE, "gemm: passes must be 1 or 3");
-  tc::GemmArgs g{M, N, K, A, sam, sak, B, sbn, sbk, D, ldd, accumulate, alpha};
-  return gemm_tf32(g, passes, (cudaStream_t)stream);
+  return gemm_tf32(M, N, K, A, sam, sak, B, sbn, sbk, D, ldd, accumulate, alpha, passes, workspace, workspace_bytes,
+                   (cudaStream_t)stream);
 }

