@@ -35,6 +35,7 @@ extern "C" {
 #define CACTO_MAX_LAYERS 5   /* affine layers per network (<= 4 hidden)        */
 #define CACTO_MAX_IN 32      /* network input width n+1                          */
 #define CACTO_MAX_OUT 8      /* network output width (control dimension m)      */
+#define CACTO_MAX_HIDDEN 1024 /* padded hidden width (32, 64, or any multiple of 32 up to this) */
 #define CACTO_MAX_OBST 4     /* elliptic obstacles of the task cost             */
 
 /* status codes */
@@ -63,8 +64,11 @@ enum cacto_score_mode { CACTO_SCORE_STD = 0, CACTO_SCORE_GAP = 1, CACTO_SCORE_ST
  *                   | W_last [out][hp] b_last [out]
  *   n_layers == 1:  W0 [out][ip] b0 [out]
  * with ip = cacto_padded_in(in) (8/16/32) and every hidden width padded to hp
- * (32 or 64).  Padding entries are zero and stay zero under the optimizer, so
- * the padded network computes exactly the reference network.
+ * (32 or 64: fused SIMT kernels, fp32 or fp64; any larger multiple of 32 up to
+ * CACTO_MAX_HIDDEN: the layer-wise tcgen05 path, fp32 only, whose workspace-free
+ * entry points use a library-owned per-device scratch).  Padding entries are
+ * zero and stay zero under the optimizer, so the padded network computes
+ * exactly the reference network.
  * ------------------------------------------------------------------------- */
 typedef struct cacto_mlp {
   int32_t dtype;
@@ -192,7 +196,11 @@ int cacto_ring_push(const cacto_batch_t* src, void* ring_xa, void* ring_u, void*
  *   critic: nets.critic_loss, nets.py:233-290 (target may be NULL)
  *   actor:  nets.actor_loss, nets.py:293-334 (rows with t >= t_max skipped;
  *           live-row count written to `live_rows` [1] int64 device)
- *   std:    nets.std_critic_loss, nets.py:337-353 */
+ *   std:    nets.std_critic_loss, nets.py:337-353
+ * Wide networks (hp > 64) are differentiated layer by layer on the tensor
+ * cores and always report n_partials = 1.  For cacto_actor_loss pass
+ * cacto_loss_workspace_bytes(actor) + cacto_loss_workspace_bytes(critic) so the
+ * critic's value/state-gradient at x' also runs inside the caller's workspace. */
 size_t cacto_loss_workspace_bytes(const cacto_mlp_t* net, int64_t rows);
 int cacto_critic_loss(const cacto_mlp_t* critic, const cacto_mlp_t* target, const cacto_batch_t* batch,
                       double k_s, int32_t bootstrap, void* workspace, size_t workspace_bytes,

@@ -52,8 +52,10 @@ int validate_mlp(const cacto_mlp_t* m, const char* who) {
     return set_error(CACTO_EUNSUPPORTED, "%s: input width %d not supported", who, m->sizes[0]);
   int out = m->sizes[m->n_layers];
   if (out < 1 || out > CACTO_MAX_OUT) return set_error(CACTO_EUNSUPPORTED, "%s: output width %d not supported", who, out);
-  if (m->n_layers > 1 && m->hp != 32 && m->hp != 64)
-    return set_error(CACTO_EUNSUPPORTED, "%s: padded hidden width %d not built", who, m->hp);
+  if (m->n_layers > 1 && m->hp != 32 && m->hp != 64 && (m->hp % 32 || m->hp > CACTO_MAX_HIDDEN))
+    return set_error(CACTO_EUNSUPPORTED, "%s: padded hidden width %d not supported", who, m->hp);
+  if (m->n_layers > 1 && m->hp > 64 && m->dtype != CACTO_F32)
+    return set_error(CACTO_EUNSUPPORTED, "%s: padded hidden width %d > 64 runs in fp32 only", who, m->hp);
   for (int i = 1; i < m->n_layers; ++i)
     if (m->sizes[i] < 1 || m->sizes[i] > m->hp)
       return set_error(CACTO_EVALUE, "%s: hidden width %d exceeds padded width %d", who, m->sizes[i], m->hp);

@@ -231,12 +231,20 @@ static int forward_entry(const cacto_mlp_t* m, const void* xa, int64_t B, void* 
 using namespace cacto;
 
 int validate_mlp(const cacto_mlp_t* m, const char* who);  // abi.cu
+namespace cacto {  // wide.cu (padded hidden width > 64)
+bool is_wide(const cacto_mlp_t* m);
+int wide_mlp_entry(const cacto_mlp_t* m, const void* xa, int64_t B, void* value, void* jac, cudaStream_t st);
+int wide_score(int mode, const cacto_mlp_t* sn, const cacto_mlp_t* cn, const float* xa, const float* rc, int64_t N,
+               float* scores, cudaStream_t st);
+int wide_forward_rows(const cacto_mlp_t* m, const cacto_batch_t* bt, int which, float* out, cudaStream_t st);
+}  // namespace cacto
 
 extern "C" int cacto_mlp_forward(const cacto_mlp_t* mlp, const void* xa, int64_t B, void* out, void* stream) {
   int rc = validate_mlp(mlp, "mlp_forward");
   if (rc) return rc;
   if (B < 0 || (B > 0 && (!xa || !out))) return set_error(CACTO_EVALUE, "mlp_forward: bad batch");
   if (B == 0) return CACTO_OK;
+  if (is_wide(mlp)) return wide_mlp_entry(mlp, xa, B, out, nullptr, (cudaStream_t)stream);
   if (mlp->dtype == CACTO_F32) return forward_entry<float>(mlp, xa, B, out, nullptr, (cudaStream_t)stream);
   return forward_entry<double>(mlp, xa, B, out, nullptr, (cudaStream_t)stream);
 }
@@ -247,6 +255,7 @@ extern "C" int cacto_mlp_jacobian(const cacto_mlp_t* mlp, const void* xa, int64_
   if (rc) return rc;
   if (B < 0 || (B > 0 && (!xa || !value || !jac))) return set_error(CACTO_EVALUE, "mlp_jacobian: bad batch");
   if (B == 0) return CACTO_OK;
+  if (is_wide(mlp)) return wide_mlp_entry(mlp, xa, B, value, jac, (cudaStream_t)stream);
   if (mlp->dtype == CACTO_F32) return forward_entry<float>(mlp, xa, B, value, jac, (cudaStream_t)stream);
   return forward_entry<double>(mlp, xa, B, value, jac, (cudaStream_t)stream);
 }
@@ -299,6 +308,9 @@ extern "C" int cacto_score(int32_t mode, const cacto_mlp_t* std_net, const cacto
     return set_error(CACTO_EVALUE, "score: std and critic nets must share dtype / widths");
   if (N < 0) return set_error(CACTO_EVALUE, "score: N < 0");
   if (N == 0) return CACTO_OK;
+  if (is_wide(need_std ? std_net : critic))
+    return wide_score(mode, need_std ? std_net : nullptr, need_crit ? critic : nullptr, (const float*)xa,
+                      (const float*)rollout_cost, N, (float*)scores, (cudaStream_t)stream);
   int dtype = need_std ? std_net->dtype : critic->dtype;
   if (dtype == CACTO_F32)
     return score_entry<float>(mode, need_std ? std_net : nullptr, need_crit ? critic : nullptr, xa, rollout_cost, N,
@@ -398,6 +410,7 @@ int cacto_forward_rows(const cacto_mlp_t* mlp, const cacto_batch_t* b, int which
   if (mlp->sizes[mlp->n_layers] != 1) return set_error(CACTO_EVALUE, "forward_rows: scalar network required");
   if (mlp->sizes[0] != b->n + 1) return set_error(CACTO_EVALUE, "forward_rows: input dim mismatch");
   if (b->rows == 0) return CACTO_OK;
+  if (is_wide(mlp)) return wide_forward_rows(mlp, b, which, (float*)out, (cudaStream_t)stream);
   if (mlp->dtype == CACTO_F32) return rows_entry<float>(mlp, b, which, out, (cudaStream_t)stream);
   return rows_entry<double>(mlp, b, which, out, (cudaStream_t)stream);
 }

@@ -567,6 +567,16 @@ __global__ void count_live_kernel(const int64_t* idx, const int64_t* cycle, int6
 using namespace cacto;
 
 int validate_mlp(const cacto_mlp_t* m, const char* who);  // abi.cu
+namespace cacto {  // wide.cu (padded hidden width > 64: layer-wise tcgen05 path)
+bool is_wide(const cacto_mlp_t* m);
+size_t wide_workspace_bytes(const cacto_mlp_t* m, int64_t rows);
+int wide_critic_loss(const cacto_mlp_t* cm, const cacto_mlp_t* tm, const cacto_batch_t* bt, double k_s, int boot,
+                     void* ws, size_t ws_bytes, cudaStream_t st);
+int wide_std_loss(const cacto_mlp_t* sm, const cacto_mlp_t* cm, const cacto_batch_t* bt, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
+int wide_actor_loss(const cacto_mlp_t* am, const cacto_mlp_t* cm, const cacto_system_t* sys, const cacto_cost_t* cost,
+                    const cacto_batch_t* bt, const int64_t* live, void* ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace cacto
 int cacto_forward_rows(const cacto_mlp_t* mlp, const cacto_batch_t* rows_of, int which, void* out,
                        void* stream);  // forward.cu helper (gathered rows)
 
@@ -581,6 +591,7 @@ static constexpr int critic_S() { return sizeof(T) == 4 ? 64 : 32; }
 
 extern "C" size_t cacto_loss_workspace_bytes(const cacto_mlp_t* net, int64_t rows) {
   if (!net) return 0;
+  if (is_wide(net)) return wide_workspace_bytes(net, rows);
   size_t es = net->dtype == CACTO_F32 ? 4 : 8;
   LayerOffsets lo = layer_offsets(shape_of(*net));
   size_t slots = (size_t)num_sms() * (size_t)(lo.total + 1) * es;
@@ -655,6 +666,11 @@ extern "C" int cacto_critic_loss(const cacto_mlp_t* critic, const cacto_mlp_t* t
   if (workspace_bytes < cacto_loss_workspace_bytes(critic, batch->rows))
     return set_error(CACTO_EVALUE, "critic_loss: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
+  if (is_wide(critic)) {
+    *n_partials = 1;
+    return wide_critic_loss(critic, bootstrap ? target : nullptr, batch, k_s, bootstrap, workspace, workspace_bytes,
+                            st);
+  }
   if (critic->dtype == CACTO_F32)
     return critic_entry<float>(critic, target, batch, k_s, bootstrap, workspace, n_partials, st);
   return critic_entry<double>(critic, target, batch, k_s, bootstrap, workspace, n_partials, st);
@@ -718,6 +734,10 @@ extern "C" int cacto_std_loss(const cacto_mlp_t* std_net, const cacto_mlp_t* cri
   if (workspace_bytes < cacto_loss_workspace_bytes(std_net, batch->rows))
     return set_error(CACTO_EVALUE, "std_loss: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
+  if (is_wide(std_net)) {
+    *n_partials = 1;
+    return wide_std_loss(std_net, critic, batch, workspace, workspace_bytes, st);
+  }
   int grid = 0;
   NetShape sh = shape_of(*std_net);
   int S = std_net->dtype == CACTO_F32 ? 64 : 32;
@@ -822,6 +842,10 @@ extern "C" int cacto_actor_loss(const cacto_mlp_t* actor, const cacto_mlp_t* cri
   if (workspace_bytes < cacto_loss_workspace_bytes(actor, batch->rows))
     return set_error(CACTO_EVALUE, "actor_loss: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
+  if (is_wide(actor)) {
+    *n_partials = 1;
+    return wide_actor_loss(actor, critic, sys, cost, batch, live_rows, workspace, workspace_bytes, st);
+  }
   if (actor->dtype == CACTO_F32)
     return actor_entry<float>(actor, critic, sys, cost, batch, live_rows, workspace, n_partials, st);
   return actor_entry<double>(actor, critic, sys, cost, batch, live_rows, workspace, n_partials, st);

@@ -67,13 +67,18 @@ def padded_in(d: int) -> int:
     return 8 if d <= 8 else (16 if d <= 16 else 32)
 
 
+MAX_HIDDEN = 1024   # CACTO_MAX_HIDDEN
+
+
 def padded_hidden(widths) -> int:
     w = max(widths) if widths else 0
     if w <= 32:
         return 32
     if w <= 64:
         return 64
-    raise ValueError(f"hidden width {w} > 64 is not built into libcacto_b200 (round-1 kernels)")
+    if w <= MAX_HIDDEN:
+        return (w + 31) // 32 * 32     # layer-wise tcgen05 path (fp32), csrc/wide.cu
+    raise ValueError(f"hidden width {w} > {MAX_HIDDEN} is not supported by libcacto_b200")
 
 
 def layer_layout(sizes, hp):

@@ -72,7 +72,8 @@ class UpdateEngine:
         L = _lib.load()
         B = self.B
         self.ws_c = torch.empty(L.cacto_loss_workspace_bytes(self.critic.dn.desc, B), device=dev, dtype=torch.uint8)
-        self.ws_a = torch.empty(L.cacto_loss_workspace_bytes(self.actor.dn.desc, B), device=dev, dtype=torch.uint8)
+        self.ws_a = torch.empty(L.cacto_loss_workspace_bytes(self.actor.dn.desc, B)
+                                + L.cacto_loss_workspace_bytes(self.critic.dn.desc, B), device=dev, dtype=torch.uint8)
         self.ws_s = torch.empty(L.cacto_loss_workspace_bytes(self.std.dn.desc, B), device=dev, dtype=torch.uint8)
         self.live = torch.zeros(1, device=dev, dtype=torch.int64)
         self.cnt = torch.zeros(2, device=dev, dtype=torch.int64)   # [critic/actor cycle, std cycle]

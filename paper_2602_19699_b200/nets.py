@@ -200,11 +200,15 @@ class _Batch:
             [c.data_ptr() for c in self.cols]
 
 
-def _run_loss(net: DeviceNet, launch):
-    """Allocate the workspace, run the loss launcher, fold the partials."""
+def _run_loss(net: DeviceNet, launch, also=()):
+    """Allocate the workspace, run the loss launcher, fold the partials.  `also`:
+    nets evaluated inside the loss whose workspace is added (the critic of the
+    actor loss, include/cacto_b200.h)."""
     dev = device()
     rows = launch.rows
-    nbytes = _lib.load().cacto_loss_workspace_bytes(net.desc, rows)
+    L = _lib.load()
+    nbytes = L.cacto_loss_workspace_bytes(net.desc, rows) + sum(L.cacto_loss_workspace_bytes(n.desc, rows)
+                                                                 for n in also)
     ws = torch.empty(nbytes, device=dev, dtype=torch.uint8)
     import ctypes
     npart = ctypes.c_int32(0)
@@ -271,7 +275,7 @@ def actor_loss(actor, critic, model, field, states):
         _lib.call("cacto_actor_loss", net.desc, cn.desc, sysd, costd, b.desc, live_t.data_ptr(),
                   ws.data_ptr(), nbytes, npart, _stream())
     launch.rows = b.desc.rows
-    loss, grads = _run_loss(net, launch)
+    loss, grads = _run_loss(net, launch, also=(cn,))
     return loss, grads, skipped
 
 
