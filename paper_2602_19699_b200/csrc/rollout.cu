@@ -11,81 +11,10 @@
 #include <stdlib.h>
 
 #include "net.cuh"
+#include "rollout.cuh"
 #include "systems.cuh"
 
 namespace cacto {
-
-template <typename T>
-struct RolloutArgs {
-  SysDev<T> sys;
-  CostDev<T> cost;
-  NetConst<T> nc;
-  int has_cost;
-  int nh, out, act, head;
-  const T* params;
-  const double* x0;
-  const int32_t* t0;
-  int t0_scalar;
-  int64_t N;
-  int t_hor;      // > 0 fixed horizon; 0 -> per-start t_max - t0
-  int t_stride;   // row stride of the per-step outputs
-  T* U;
-  T* X;
-  T* SC;
-  T* C;
-};
-
-// NumPy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) for
-// n <= 128 terms, fed one term at a time.  Longer sums chain 128-blocks.
-template <typename T>
-struct PairwiseSum {
-  T r[8];
-  T res;
-  int n;  // total terms
-  CACTO_D void init(int n_) {
-    n = n_;
-    res = T(0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = T(0);
-  }
-  CACTO_D static T combine(const T (&r)[8]) {
-    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  }
-  CACTO_D void add(int i, T v) {
-    if (n < 8) {
-      res += v;
-      return;
-    }
-    if (n > 128) {  // chained blocks of 128 (not bit-exact beyond 128 terms)
-      int blk = i >> 7, off = i & 127;
-      int len = min(128, n - (blk << 7));
-      if (off == 0) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = T(0);
-      }
-      sub(off, len, v, blk > 0);
-      return;
-    }
-    sub(i, n, v, false);
-  }
-  CACTO_D void sub(int i, int len, T v, bool chain) {
-    int body = len - (len % 8);
-    if (len < 8) {
-      res += v;
-      return;
-    }
-    if (i < body) {
-      int j = i & 7;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q == j) r[q] = (i < 8) ? v : r[q] + v;
-      if (i == body - 1 && body == len) res = chain ? res + combine(r) : combine(r);
-    } else {
-      if (i == body) res = chain ? res + combine(r) : combine(r);
-      res += v;
-    }
-  }
-};
 
 // S starts per CTA; TM = 8 (8x8 micro-tiles, 1 CTA / SM) for the 256-start
 // tile, TM = 4 otherwise
@@ -213,9 +142,16 @@ static int tile_override() {
   return v;
 }
 
+// rollout_tc.cu: the tensor-core rollout (fp32, n + 1 <= 16, 1..3 hidden layers)
+template <int SYS, int HP>
+int launch_rollout_tc(const RolloutArgs<float>& a, cudaStream_t st);
+bool rollout_tc_enabled();
+
 template <typename T, int SYS, int HP>
 static int launch_rollout(const RolloutArgs<T>& a, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
+    if (rollout_tc_enabled() && a.nh >= 1 && a.nh <= 3 && SysDims<SYS>::n + 1 <= 16 && SysDims<SYS>::m <= 8)
+      return launch_rollout_tc<SYS, HP>(a, st);
     // 128-start tiles (2 CTAs / SM, 4x8 micro-tiles) measured faster than 256-start
     // tiles (1 CTA / SM, 8x8) on B200: 4.13 vs 4.57 ms (profiles/README.md)
     const int ov = tile_override();

@@ -8,6 +8,8 @@
 // MN-major operands.  Gradients are written in the padded parameter layout into
 // workspace slot 0 (n_partials = 1), with the loss at index P, so the existing
 // fold / Adam kernels apply unchanged.  Deterministic: no atomics.
+#include <cstdlib>
+
 #include "net.cuh"
 #include "systems.cuh"
 
@@ -464,23 +466,35 @@ static RowSrc batch_src(const cacto_batch_t* b, const void* col, int64_t stride)
 // ======================================================================================
 using namespace wide;
 
-bool is_wide(const cacto_mlp_t* m) { return m && m->n_layers > 1 && m->hp > 64; }
+// CACTO_WIDE_MIN=<w> moves the layer-wise path's threshold down (measurement aid:
+// fp32 nets with hp >= w take it; default: hp > 64 only)
+static int wide_min() {
+  static int v = [] {
+    const char* e = getenv("CACTO_WIDE_MIN");
+    return e ? atoi(e) : 65;
+  }();
+  return v;
+}
+bool is_wide(const cacto_mlp_t* m) {
+  return m && m->n_layers > 1 && (m->hp > 64 || (m->dtype == CACTO_F32 && m->hp >= wide_min()));
+}
 
+// one network's loss / Jacobian workspace: gradient slot, per-layer Z / A / G,
+// two [B][H] scratch matrices, the [B][ip] input / sweep / cotangent tiles, the
+// per-row vectors, column-sum and loss partials and the split-K partials
 size_t wide_workspace_bytes(const cacto_mlp_t* m, int64_t rows) {
   if (!is_wide(m)) return 0;
   NetShape sh = shape_of(*m);
-  const int64_t B = rows > 0 ? rows : 1;
-  const int H = sh.hp, nh = sh.nh;
+  const size_t B = (size_t)(rows > 0 ? rows : 1);
+  const size_t H = (size_t)sh.hp, nh = (size_t)sh.nh;
   LayerOffsets lo = layer_offsets(sh);
-  size_t f = 0;
-  f += (size_t)(lo.total + 1) + 64;                        // gradient slot
-  f += (size_t)2 * ((size_t)B * sh.ip + 3 * (size_t)nh * B * H + (size_t)B * 8);  // two nets' activations
-  f += (size_t)3 * B * H;                                  // S / R / U / ABAR scratch
-  f += (size_t)4 * B * 32 + 8 * (size_t)B;                 // S0, U0, DEL, XN, per-row vectors
-  f += (size_t)kRedRows * (H > 32 ? H : 32) + 4096;        // column partials, loss partials
-  size_t g = gemm_workspace_bytes(H, H, (int)B);
-  size_t g2 = gemm_workspace_bytes(H, 32, (int)B);
-  return f * 4 + (g > g2 ? g : g2) + 64 * 256;
+  size_t f = (size_t)(lo.total + 1);
+  f += 3 * B * sh.ip + 3 * nh * B * H + 2 * B * H;  // X0 S0 U0 | Z A G | R0 R1 (S, ABAR)
+  f += 8 * B + 8 * B + 2 * 32 * B + 4 * B;           // O, DEL, XN / GN, per-row vectors
+  f += (size_t)kRedRows * (H > 32 ? H : 32) + 1024 + 64 * 32;  // partials + arena alignment slack
+  size_t g = gemm_workspace_bytes((int)H, (int)H, (int)B);
+  size_t g2 = gemm_workspace_bytes((int)H, 32, (int)B);
+  return f * 4 + (g > g2 ? g : g2) + 256;
 }
 
 static Ctx make_ctx(Arena& ar, int H, int64_t B, cudaStream_t st) {
