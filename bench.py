@@ -208,6 +208,9 @@ def cpu_model():
 # GPU arm
 # ---------------------------------------------------------------------------------
 
+TF32_DENSE_TFLOPS = 1100.0   # /opt/skills/guides/B200_PROFILING.md peak table (dense tf32)
+
+
 def measure_fp32_peak(torch, _lib, stream):
     """FFMA throughput of this B200 (roofline denominator of the SIMT kernels)."""
     blocks = 148 * 8
@@ -375,7 +378,19 @@ def main():
         evs.append(a.elapsed_time(b))
     roll_ms = float(np.mean(evs))
     achieved = f_roll * N / (roll_ms * 1e-3) / 1e12
-    peak = measure_fp32_peak(torch, _lib, stream)
+    ffma_peak = measure_fp32_peak(torch, _lib, stream)
+    tc_path = args.precision == "fp32" and os.environ.get("CACTO_ROLLOUT_TC", "1") != "0"
+    if tc_path:
+        # K1 runs its policy layers on tcgen05 (kind::tf32, 3 MMA passes for fp32
+        # accuracy): the roofline is the TF32 tensor pipe
+        peak, bound = TF32_DENSE_TFLOPS, "tensor"
+        peak_source = ("B200_PROFILING.md fallback: tf32 dense 1.1 PFLOP/s (MEASURED_PEAKS.json has no tf32 "
+                       "entry); algorithmic flops count each product once, the 3xTF32 split issues 3x")
+        kname = "rollout_tc_kernel (K1 on tcgen05, cost-only over all candidates)"
+    else:
+        peak, bound = ffma_peak, "fp32_simt"
+        peak_source = "measured FFMA throughput on this GPU (cacto_fma_peak); MEASURED_PEAKS.json has no fp32 entry"
+        kname = "rollout_kernel (K1 SIMT, cost-only over all candidates)"
     traffic = None
     prof = ROOT / "profiles" / "rollout_ncu_summary.json"
     if prof.exists():
@@ -396,12 +411,12 @@ def main():
                    "parallelism": f"shard-by-candidate x{world}"},
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches_per_step * args.steps,
-        "roofline": {"bound": "fp32_simt", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "kernel": "rollout_kernel (K1, cost-only over all candidates)",
-                     "kernel_ms": roll_ms, "flops_per_candidate_rollout": f_roll,
-                     "peak_source": "measured FFMA throughput on this GPU (cacto_fma_peak); "
-                                    "MEASURED_PEAKS.json has no fp32 entry"},
+                     "kernel": kname, "kernel_ms": roll_ms, "flops_per_candidate_rollout": f_roll,
+                     "peak_source": peak_source,
+                     "mma_passes": 3 if tc_path else None,
+                     "fp32_ffma_peak": ffma_peak, "vs_ffma_peak": achieved / ffma_peak if ffma_peak else None},
         "clocks": clk,
         "flops_per_candidate": f_cand,
         "achieved_tflops_step": f_cand * N / (ms * 1e-3) / 1e12,

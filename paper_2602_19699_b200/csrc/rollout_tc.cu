@@ -1,24 +1,31 @@
 // rollout_tc.cu -- K1 on the tensor cores: the fused closed-loop actor rollout
 // (nets.actor_rollout, nets.py:403-423) with every policy layer issued as
-// tcgen05.mma (kind::tf32, 3xTF32 for fp32 accuracy) into TMEM, and the
-// activation / head / dynamics / running-cost work done by the thread that owns
-// the start.
+// tcgen05.mma and the activation / head / dynamics / running-cost work done by
+// the thread that owns the start.
+//
+// Arithmetic: fp32 results from fp16 tensor-core products ("3xFP16"): every
+// operand x = hi + lo with hi = fp16(x), lo = fp16(x - hi) (11 + 11 significant
+// bits), and each layer issues hi*hi + hi*lo + lo*hi with fp32 accumulation --
+// the precision of the 3xTF32 split at twice the MMA rate (kind::f16, K = 16 per
+// instruction).  Weights are pre-scaled by powers of two (and log2 e for ELU) so
+// their lo parts stay normal fp16 numbers.
 //
 // CTA = NT tiles of 128 starts (TMEM lane = start) + one MMA warp.
-//   TMEM per tile (2*HP columns): D [HP] accumulator | A_hi [HP] activations.
-//   Shared memory: weights (hi and lo, K-major SW128) for the whole horizon, and
-//   per tile the A_lo activations (K-major SW128).
-//   Per layer and tile the MMA warp issues, for each k-step of 8,
-//       D += A_hi(TMEM) W_hi + A_hi(TMEM) W_lo + A_lo(smem) W_hi
-//   (3xTF32: x = hi + lo with hi = rna_tf32(x)) and commits to the tile's
-//   mbarrier.  The tile's 4 epilogue warps (warp w -> TMEM lanes 32(w%4)..+31)
-//   then tcgen05.ld the D row, add the bias, apply the activation, write hi back
-//   to TMEM (tcgen05.st) and lo to shared memory, and arrive.  After the output
-//   layer the owner thread applies the head, accumulates the stage cost in
-//   NumPy's pairwise order, steps the dynamics and writes the next normalised
-//   input row.
-// The NT tiles are in flight together, so one tile's epilogue overlaps the other
-// tiles' MMAs and hand-off latencies.  Nothing but the outputs touches HBM.
+//   TMEM per tile (2*HP columns): D [HP] fp32 accumulator | A_hi [HP/2] | A_lo
+//   [HP/2] (fp16 pairs).  Shared memory holds only the weights (hi/lo, K-major
+//   SW128) and the scaled biases, for the whole horizon.
+//   Per layer and tile the MMA warp issues, for each k-step of 16, the three
+//   products with A read from TMEM, and commits to the tile's mbarrier.  The
+//   tile's epilogue warps (warp w -> TMEM lanes 32(w%4)..+31) tcgen05.ld the D
+//   row, apply the activation, tcgen05.st the split activations as the next
+//   layer's A, pre-load D with the next layer's bias, and arrive.  After the
+//   output layer the owner thread applies the head, accumulates the stage cost
+//   in NumPy's pairwise order, steps the dynamics and writes the next input.
+//
+// ELU layers: the accumulator holds D = 8 log2(e) z, so
+// ELU(z) = max(D,0)/(8 log2 e) + (ex2(min(D,0)/8) - 1): two FMNMX, one FMUL, one
+// MUFU, one FADD, one FFMA per element, branch-free.
+#include <cuda_fp16.h>
 #include <stdlib.h>
 
 #include "net.cuh"
@@ -31,90 +38,126 @@ namespace cacto {
 namespace rtc {
 
 constexpr int TILE = 128;
-constexpr int NOUT = 16;  // output-layer MMA width (m <= 8 used)
+constexpr int NOUT = 16;        // output-layer MMA width (m <= 8 used)
+constexpr int KIN = 16;         // input-layer K (n + 1 <= 16, zero padded)
+constexpr float WSCALE = 8.f;   // 2^3 weight pre-scale
+constexpr float LOG2E = 1.4426950408889634f;
 
-CACTO_HD constexpr int kin_of(int n) { return ((n + 1) + 7) / 8 * 8; }  // input K (8 or 16)
-
-// shared-memory plan (bytes, from a 1024-aligned base)
-template <int HP, int NT>
+// shared-memory plan (bytes, from a 1024-aligned base); fp16 K-major SW128
+// operands: rows of 128 B = 64 halves
+template <int HP>
 struct Plan {
-  static constexpr int KB = HP / 32;                // 32-wide K blocks of a hidden operand
-  static constexpr uint32_t ALO = KB * TILE * 128;  // per tile: A_lo [128][HP] SW128
-  static constexpr uint32_t W0 = HP * 128;          // [HP][32] one block
-  static constexpr uint32_t WH = KB * HP * 128;     // [HP][HP]
-  static constexpr uint32_t WO = KB * NOUT * 128;   // [16][HP]
-  static constexpr uint32_t off_alo(int t) { return t * ALO; }
-  static constexpr uint32_t off_w0 = NT * ALO;          // hi, lo
-  static constexpr uint32_t off_wh = off_w0 + 2 * W0;   // (hi, lo) x (nh - 1), nh <= 3
+  static constexpr uint32_t W0 = HP * 128;    // [HP][16 used]
+  static constexpr uint32_t WH = HP * 128;    // [HP][HP]   (HP <= 64)
+  static constexpr uint32_t WO = NOUT * 128;  // [16][HP]
+  static constexpr uint32_t off_w0 = 0;       // hi, lo
+  static constexpr uint32_t off_wh = off_w0 + 2 * W0;  // (hi, lo) x (nh - 1), nh <= 3
   static constexpr uint32_t off_wo = off_wh + 2 * 2 * WH;
-  static constexpr uint32_t off_bias = off_wo + 2 * WO;  // fp32 [3][HP] + [NOUT]
+  static constexpr uint32_t off_bias = off_wo + 2 * WO;  // fp32 [3][HP] + [NOUT], scaled
   static constexpr uint32_t bytes = off_bias + (3 * HP + NOUT) * 4 + 1024;
-  static constexpr uint32_t TMEM_COLS = NT * 2 * HP <= 128 ? 128 : (NT * 2 * HP <= 256 ? 256 : 512);
-  static_assert(NT * 2 * HP <= 512, "TMEM: 2*HP columns per tile");
+};
+template <int HP, int NT>
+struct Tmem {
+  static constexpr uint32_t PER_TILE = 2 * HP;  // D | A_hi | A_lo
+  static constexpr uint32_t COLS = NT * PER_TILE <= 128 ? 128 : (NT * PER_TILE <= 256 ? 256 : 512);
+  static_assert(NT * PER_TILE <= 512, "TMEM: 2*HP columns per tile");
 };
 
-// byte offset of element (r, c) in a K-major SW128 operand of `rows` rows
-CACTO_HD uint32_t sw128(int rows, int r, int c) {
-  const int kb = c >> 5, cc = c & 31;
-  return (uint32_t)(kb * rows * 128 + r * 128 + ((((cc >> 2) ^ (r & 7))) << 4) + (cc & 3) * 4);
+// byte offset of fp16 element (r, k) in a K-major SW128 operand (k < 64)
+CACTO_HD uint32_t sw128h(int r, int k) {
+  return (uint32_t)(r * 128 + ((((k * 2) >> 4) ^ (r & 7)) << 4) + ((k * 2) & 15));
 }
 
-// stage a row-major [rows][cols] (stride) fp32 matrix as hi/lo K-major SW128
-// operands of `rrows` x kcols (zero padded)
+CACTO_D uint32_t pack_h2(float lo_k, float hi_k) {  // low half = even k
+  __half2 h = __floats2half2_rn(lo_k, hi_k);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// x = hi + lo, both fp16, for a pair of consecutive k
+CACTO_D void split2(float v0, float v1, uint32_t& hi, uint32_t& lo) {
+  __half2 h = __floats2half2_rn(v0, v1);
+  const float2 hf = __half22float2(h);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = pack_h2(v0 - hf.x, v1 - hf.y);
+}
+
+// stage W (row-major [rows][cols], stride) * scale as hi/lo fp16 K-major SW128
+// operands of rrows x kcols (zero padded); kcols <= 64
 CACTO_D void stage_w(unsigned char* hi, unsigned char* lo, const float* src, int rows, int cols, int stride,
-                     int rrows, int kcols, int tid, int nthr) {
+                     float scale, int rrows, int kcols, int tid, int nthr) {
   for (int e = tid; e < rrows * kcols; e += nthr) {
     const int r = e / kcols, c = e - r * kcols;
-    const float v = (r < rows && c < cols) ? src[(int64_t)r * stride + c] : 0.f;
-    const uint32_t o = sw128(rrows, r, c);
-    const float vh = tc::tf32_rna(v);
-    *reinterpret_cast<float*>(hi + o) = vh;
-    *reinterpret_cast<float*>(lo + o) = v - vh;
+    const float v = (r < rows && c < cols) ? src[(int64_t)r * stride + c] * scale : 0.f;
+    const __half h = __float2half_rn(v);
+    const uint32_t o = sw128h(r, c);
+    *reinterpret_cast<__half*>(hi + o) = h;
+    *reinterpret_cast<__half*>(lo + o) = __float2half_rn(v - __half2float(h));
   }
 }
 
-// one layer of one tile: KSTEPS k-steps of hi*hi + hi*lo + lo*hi; later k-steps'
-// descriptors are the base descriptors plus constant start offsets (16-B units)
-template <int KSTEPS, int WROWS>
-CACTO_D void issue_layer(uint32_t dcol, uint32_t ahi_t, uint64_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc) {
+// scaled bias of one layer: scale * (b - shift * rowsum(W)) over the real columns
+CACTO_D void stage_bias(float* dst, const float* W, const float* b, int rows, int cols, int stride, float scale,
+                        bool shift, int rrows, int tid, int nthr) {
+  for (int r = tid; r < rrows; r += nthr) {
+    float v = 0.f;
+    if (r < rows) {
+      float s = 0.f;
+      if (shift)
+        for (int c = 0; c < cols; ++c) s += W[(int64_t)r * stride + c];
+      v = scale * (b[r] - s);
+    }
+    dst[r] = v;
+  }
+}
+
+// one layer of one tile: KSTEPS k-steps of hi*hi + hi*lo + lo*hi (A from TMEM);
+// D was pre-loaded with the bias, so every MMA accumulates
+template <int KSTEPS>
+CACTO_D void issue_layer(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc) {
 #pragma unroll
   for (int kk = 0; kk < KSTEPS; ++kk) {
-    const uint64_t ao = (uint64_t)((((kk >> 2) * TILE * 128) + (kk & 3) * 32) >> 4);
-    const uint64_t wo = (uint64_t)((((kk >> 2) * WROWS * 128) + (kk & 3) * 32) >> 4);
-    tc::mma_tf32_ts_elect(dcol, ahi_t + (uint32_t)(kk * 8), whi + wo, idesc, kk > 0 ? 1u : 0u);
-    tc::mma_tf32_ts_elect(dcol, ahi_t + (uint32_t)(kk * 8), wlo + wo, idesc, 1u);
-    tc::mma_tf32_elect(dcol, alo + ao, whi + wo, idesc, 1u);
+    const uint64_t wo = (uint64_t)(kk * 2);  // 32 bytes = 16 halves, in 16-byte units
+    const uint32_t ao = (uint32_t)(kk * 8);  // 16 halves = 8 TMEM columns
+    tc::mma_f16_ts_elect(d, ahi + ao, whi + wo, idesc, 1u);
+    tc::mma_f16_ts_elect(d, ahi + ao, wlo + wo, idesc, 1u);
+    tc::mma_f16_ts_elect(d, alo + ao, whi + wo, idesc, 1u);
   }
 }
 
 }  // namespace rtc
 
-// branch-free forward activation (ELU through the SFU exponential, like the SIMT
-// path's act_fast); straight-line code lets the scheduler interleave columns
 template <int ACT>
-CACTO_D float act_tc(float z) {
-  if constexpr (ACT == CACTO_ACT_ELU) {
-    const float e = tc::ex2_ftz(fminf(z, 0.f) * 1.4426950408889634f) - 1.f;
-    return z > 0.f ? z : e;
+struct ActTC {
+  // hidden/input layers: D = S * z (ELU: S = 8 log2 e, tanh: S = 8)
+  static constexpr float S = ACT == CACTO_ACT_ELU ? rtc::WSCALE * rtc::LOG2E : rtc::WSCALE;
+  // (feeding ELU(z) + 1 forward and folding the -1 into the next bias saves one
+  // FADD per element but adds ~2^-22 absolute error to every activation near 0:
+  // 5x the output error in an fp64 emulation, so the shift is not used)
+  static constexpr bool SHIFT = false;
+  CACTO_D static float apply(float d) {
+    if constexpr (ACT == CACTO_ACT_ELU) {
+      const float e = tc::ex2_ftz(fminf(d, 0.f) * (1.f / rtc::WSCALE)) - 1.f;
+      return fmaf(fmaxf(d, 0.f), 1.f / S, e);
+    } else {
+      return tanhf(d * (1.f / S));
+    }
   }
-  return tanhf(z);
-}
+};
 
 template <int SYS, int HP, int NT, int SPLIT, int ACT>
 __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(const RolloutArgs<float> a) {
   using namespace rtc;
-  using PL = Plan<HP, NT>;
+  using PL = Plan<HP>;
+  using TM = Tmem<HP, NT>;
+  using AF = ActTC<ACT>;
   constexpr int n = SysDims<SYS>::n;
   constexpr int m = SysDims<SYS>::m;
-  constexpr int KIN = kin_of(n);
   constexpr int IP = (n + 1) <= 8 ? 8 : ((n + 1) <= 16 ? 16 : 32);  // padded W0 row stride
-  constexpr int WPT = 4 * SPLIT;       // epilogue warps per tile (SPLIT per TMEM lane quadrant)
-  constexpr int COLS = HP / SPLIT;     // hidden columns per epilogue warp
-  constexpr int CH = COLS < 32 ? COLS : 32;
+  constexpr int WPT = 4 * SPLIT;    // epilogue warps per tile (SPLIT per TMEM lane quadrant)
+  constexpr int COLS = HP / SPLIT;  // accumulator columns per epilogue warp
   constexpr int NTHR = NT * WPT * 32 + 32;
   constexpr int MMA_WARP = NT * WPT;
-  static_assert(COLS >= 16, "at least 16 columns per epilogue warp");
-  static_assert(KIN <= 16 && m <= 8, "tensor-core rollout: n + 1 <= 16, m <= 8");
+  static_assert(n + 1 <= KIN && m <= 8 && HP <= 64, "tensor-core rollout: n + 1 <= 16, m <= 8, HP <= 64");
+  static_assert(COLS == 16 || COLS == 32 || COLS == 64, "16, 32 or 64 columns per epilogue warp");
 
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
@@ -125,22 +168,24 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nh = a.nh;
 
-  // ---- weights -> shared memory (hi/lo, SW128), biases (fp32) ----------------------
+  // ---- weights -> shared memory (scaled, hi/lo fp16, SW128), scaled biases ---------
   {
     const float* P = a.params;
     const int64_t b0 = (int64_t)HP * IP;
-    stage_w(base + PL::off_w0, base + PL::off_w0 + PL::W0, P, HP, n + 1, IP, HP, 32, threadIdx.x, NTHR);
     float* bias = reinterpret_cast<float*>(base + PL::off_bias);
-    for (int c = threadIdx.x; c < HP; c += NTHR) bias[c] = P[b0 + c];
+    stage_w(base + PL::off_w0, base + PL::off_w0 + PL::W0, P, HP, n + 1, IP, AF::S, HP, KIN, threadIdx.x, NTHR);
+    stage_bias(bias, P, P + b0, HP, n + 1, IP, AF::S, false, HP, threadIdx.x, NTHR);
     int64_t off = b0 + HP;
     for (int i = 1; i < nh; ++i) {
       unsigned char* hi = base + PL::off_wh + (uint32_t)(2 * (i - 1)) * PL::WH;
-      stage_w(hi, hi + PL::WH, P + off, HP, HP, HP, HP, HP, threadIdx.x, NTHR);
-      for (int c = threadIdx.x; c < HP; c += NTHR) bias[i * HP + c] = P[off + (int64_t)HP * HP + c];
+      stage_w(hi, hi + PL::WH, P + off, HP, HP, HP, AF::S, HP, HP, threadIdx.x, NTHR);
+      stage_bias(bias + i * HP, P + off, P + off + (int64_t)HP * HP, HP, HP, HP, AF::S, AF::SHIFT, HP, threadIdx.x,
+                 NTHR);
       off += (int64_t)HP * HP + HP;
     }
-    stage_w(base + PL::off_wo, base + PL::off_wo + PL::WO, P + off, m, HP, HP, NOUT, HP, threadIdx.x, NTHR);
-    for (int c = threadIdx.x; c < NOUT; c += NTHR) bias[3 * HP + c] = c < m ? P[off + (int64_t)m * HP + c] : 0.f;
+    stage_w(base + PL::off_wo, base + PL::off_wo + PL::WO, P + off, m, HP, HP, WSCALE, NOUT, HP, threadIdx.x, NTHR);
+    stage_bias(bias + 3 * HP, P + off, P + off + (int64_t)m * HP, m, HP, HP, WSCALE, AF::SHIFT, NOUT, threadIdx.x,
+               NTHR);
   }
   if (threadIdx.x == 0) {
     for (int t = 0; t < NT; ++t) {
@@ -150,7 +195,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     s_kmax = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MMA_WARP) tc::tmem_alloc(&tmem_base_sh, PL::TMEM_COLS);
+  if (warp == MMA_WARP) tc::tmem_alloc(&tmem_base_sh, TM::COLS);
   tc::fence_async_smem();  // staged weights -> async proxy
   tc::tc_fence_before();
   __syncthreads();
@@ -159,7 +204,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   const uint32_t sbase = saddr(base);
 
   // ---- roles: epilogue warp w < MMA_WARP serves tile g = w / WPT, TMEM lanes
-  //      32(w%4)..+31 = starts r of the tile, hidden columns [part*COLS, +COLS);
+  //      32(w%4)..+31 = starts r of the tile, accumulator columns [part*COLS, +COLS);
   //      the part-0 warp of a quadrant owns the starts' state -------------------------
   const bool epi = warp < MMA_WARP;
   const int g = warp / WPT;
@@ -189,17 +234,38 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   const int kmax = s_kmax;
 
   if (epi) {
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 2 * HP);
-    const uint32_t t_d = lane_base, t_ahi = lane_base + HP;  // this thread's D / A_hi row
-    const uint32_t alo = sbase + PL::off_alo(g);
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * TM::PER_TILE);
+    const uint32_t t_d = lane_base, t_ahi = lane_base + HP, t_alo = lane_base + HP + HP / 2;
     const uint32_t bias_s = sbase + PL::off_bias;
+    const int c_base = part * COLS;
     uint32_t pd = 0;
-    auto put_lo4 = [&](int c, float v0, float v1, float v2, float v3) {
-      sts4(alo + sw128(TILE, r, c), V4<float>{{v0, v1, v2, v3}});
+    // D[my columns] <- scaled bias of layer l (l == nh: the output layer, part 0)
+    auto preload_bias = [&](int l) {
+      if (l == nh) {
+        if (part != 0) return;
+        float b[16];
+#pragma unroll
+        for (int c = 0; c < 16; c += 4) {
+          const V4<float> v = lds4(bias_s + (uint32_t)((3 * HP + c) * 4), (float*)nullptr);
+          b[c] = v.v[0]; b[c + 1] = v.v[1]; b[c + 2] = v.v[2]; b[c + 3] = v.v[3];
+        }
+        tc::tmem_st16(t_d, b);
+        return;
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < COLS; c0 += 16) {
+        float b[16];
+#pragma unroll
+        for (int c = 0; c < 16; c += 4) {
+          const V4<float> v = lds4(bias_s + (uint32_t)((l * HP + c_base + c0 + c) * 4), (float*)nullptr);
+          b[c] = v.v[0]; b[c + 1] = v.v[1]; b[c + 2] = v.v[2]; b[c + 3] = v.v[3];
+        }
+        tc::tmem_st16(t_d + (uint32_t)(c_base + c0), b);
+      }
     };
     auto write_input = [&](int k) {
       if (part != 0) return;
-      float v[KIN], hv[KIN];
+      float v[KIN];
 #pragma unroll
       for (int c = 0; c < KIN; ++c) v[c] = 0.f;
       if (owner) {
@@ -207,18 +273,20 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
         for (int c = 0; c < n; ++c) v[c] = (x[c] - a.nc.in_center[c]) / a.nc.in_half[c];
         v[n] = ((float)(t0 + k) - a.nc.in_center[n]) / a.nc.in_half[n];
       }
+      float hv[KIN / 2], lv[KIN / 2];
 #pragma unroll
-      for (int c = 0; c < KIN; ++c) hv[c] = tc::tf32_rna(v[c]);
-      if constexpr (KIN == 8) tc::tmem_st8(t_ahi, hv);
-      else tc::tmem_st16(t_ahi, hv);
-#pragma unroll
-      for (int c = 0; c < KIN; c += 4)
-        put_lo4(c, v[c] - hv[c], v[c + 1] - hv[c + 1], v[c + 2] - hv[c + 2], v[c + 3] - hv[c + 3]);
+      for (int c = 0; c < KIN; c += 2) {
+        uint32_t h, l;
+        split2(v[c], v[c + 1], h, l);
+        hv[c / 2] = __uint_as_float(h);
+        lv[c / 2] = __uint_as_float(l);
+      }
+      tc::tmem_st8(t_ahi, hv);
+      tc::tmem_st8(t_alo, lv);
     };
     auto handoff = [&]() {
       tc::tmem_wait_st();
       tc::tc_fence_before();
-      tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full_bar[g]);
     };
@@ -229,32 +297,35 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     };
     if (kmax > 0) {
       write_input(0);
+      preload_bias(0);
       handoff();
     }
     for (int k = 0; k < kmax; ++k) {
       for (int l = 0; l < nh; ++l) {  // hidden layers
         wait_done();
 #pragma unroll
-        for (int cc0 = 0; cc0 < COLS; cc0 += CH) {
-          const int c0 = part * COLS + cc0;
-          float z[CH], hv[CH];
-          if constexpr (CH == 32) tc::tmem_ld32_wait(t_d + (uint32_t)c0, z);
-          else tc::tmem_ld16_wait(t_d + (uint32_t)c0, z);
-          const uint32_t bl = bias_s + (uint32_t)((l * HP + c0) * 4);
+        for (int c0 = 0; c0 < COLS; c0 += 32) {
+          constexpr int CH = COLS < 32 ? COLS : 32;
+          float z[CH], hv[CH / 2], lv[CH / 2];
+          if constexpr (CH == 32) tc::tmem_ld32_wait(t_d + (uint32_t)(c_base + c0), z);
+          else tc::tmem_ld16_wait(t_d + (uint32_t)(c_base + c0), z);
 #pragma unroll
-          for (int c = 0; c < CH; c += 4) {
-            const V4<float> b4 = lds4(bl + c * 4, (float*)nullptr);
-            float v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              v[j] = act_tc<ACT>(z[c + j] + b4.v[j]);
-              hv[c + j] = tc::tf32_rna(v[j]);
-            }
-            put_lo4(c0 + c, v[0] - hv[c], v[1] - hv[c + 1], v[2] - hv[c + 2], v[3] - hv[c + 3]);
+          for (int c = 0; c < CH; c += 2) {
+            uint32_t h, lo;
+            split2(AF::apply(z[c]), AF::apply(z[c + 1]), h, lo);
+            hv[c / 2] = __uint_as_float(h);
+            lv[c / 2] = __uint_as_float(lo);
           }
-          if constexpr (CH == 32) tc::tmem_st32(t_ahi + (uint32_t)c0, hv);
-          else tc::tmem_st16(t_ahi + (uint32_t)c0, hv);
+          const uint32_t ac = (uint32_t)((c_base + c0) / 2);
+          if constexpr (CH == 32) {
+            tc::tmem_st16(t_ahi + ac, hv);
+            tc::tmem_st16(t_alo + ac, lv);
+          } else {
+            tc::tmem_st8(t_ahi + ac, hv);
+            tc::tmem_st8(t_alo + ac, lv);
+          }
         }
+        preload_bias(l + 1);
         handoff();
       }
       // output layer -> head, cost, dynamics
@@ -262,10 +333,9 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       float o[16];
       if (part == 0) tc::tmem_ld16_wait(t_d, o);
       if (owner && k < T_i) {
-        const float* bias = reinterpret_cast<const float*>(base + PL::off_bias);
         float u[m];
 #pragma unroll
-        for (int j = 0; j < m; ++j) u[j] = head_value(a.head, a.nc, j, o[j] + bias[3 * HP + j]);
+        for (int j = 0; j < m; ++j) u[j] = head_value(a.head, a.nc, j, o[j] * (1.f / WSCALE));
         if (a.U) {
 #pragma unroll
           for (int j = 0; j < m; ++j) a.U[(gi * a.t_stride + k) * m + j] = u[j];
@@ -285,6 +355,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       }
       if (k + 1 < kmax) {
         write_input(k + 1);
+        preload_bias(0);
         handoff();
       }
     }
@@ -296,7 +367,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     }
   } else {
     // ---- MMA issuer (whole warp converged; elect.sync picks the issuing lane) ----------
-    const uint32_t idesc_h = tc::idesc_tf32(HP, 0, 0), idesc_o = tc::idesc_tf32(NOUT, 0, 0);
+    const uint32_t idesc_h = tc::idesc_f16(HP), idesc_o = tc::idesc_f16(NOUT);
     auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
     const uint64_t w0h = desc(PL::off_w0), w0l = desc(PL::off_w0 + PL::W0);
     const uint64_t woh = desc(PL::off_wo), wol = desc(PL::off_wo + PL::WO);
@@ -310,15 +381,14 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
           tc::mbar_wait_sleep(&full_bar[t], pf[t]);
           pf[t] ^= 1;
           tc::tc_fence_after();
-          const uint32_t dcol = tmem + (uint32_t)(t * 2 * HP), ahi = dcol + HP;
-          const uint64_t al = desc(PL::off_alo(t));
+          const uint32_t d = tmem + (uint32_t)(t * TM::PER_TILE), ahi = d + HP, alo = d + HP + HP / 2;
           if (l == 0) {
-            issue_layer<KIN / 8, HP>(dcol, ahi, al, w0h, w0l, idesc_h);
+            issue_layer<KIN / 16>(d, ahi, alo, w0h, w0l, idesc_h);
           } else if (l < nh) {
             const uint32_t wo = PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;
-            issue_layer<HP / 8, HP>(dcol, ahi, al, desc(wo), desc(wo + PL::WH), idesc_h);
+            issue_layer<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h);
           } else {
-            issue_layer<HP / 8, NOUT>(dcol, ahi, al, woh, wol, idesc_o);
+            issue_layer<HP / 16>(d, ahi, alo, woh, wol, idesc_o);
           }
           tc::tc_commit_elect(&done_bar[t]);
           __syncwarp();
@@ -328,15 +398,15 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == MMA_WARP) tc::tmem_dealloc(tmem, PL::TMEM_COLS);
+  if (warp == MMA_WARP) tc::tmem_dealloc(tmem, TM::COLS);
 }
 
 template <int SYS, int HP, int NT>
 static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
-  using PL = rtc::Plan<HP, NT>;
+  using PL = rtc::Plan<HP>;
   // 4 tiles: one epilogue warp per lane quadrant; fewer tiles: the columns are
   // split over more warps (shorter per-layer epilogue latency), 544 threads max
-  constexpr int SPLIT = (NT == 4 || HP == 32) ? 1 : 4 / NT;
+  constexpr int SPLIT = NT == 4 ? 1 : (NT == 2 ? (HP >= 32 ? 2 : 1) : (HP >= 64 ? 4 : HP / 16));
   auto kern = a.act == CACTO_ACT_ELU ? rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_ELU>
                                      : rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_TANH>;
   if (!ensure_smem((const void*)kern, PL::bytes))

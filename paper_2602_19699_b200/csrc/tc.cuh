@@ -104,6 +104,22 @@ CACTO_D void tc_commit_elect(uint64_t* bar) {
       : "memory");
 }
 
+// instruction descriptor: D f32, A/B f16 (kind::f16), both K-major, M x N
+CACTO_HD uint32_t idesc_f16(int bn, int bm = 128) {
+  return (1u << 4) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(bm >> 4) << 24);
+}
+// kind::f16 MMA with A in TMEM (two K-consecutive halves per 32-bit column,
+// low half = even k), B in shared memory; warp-converged, elect.sync issues
+CACTO_D void mma_f16_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // TMEM allocation (one warp, .sync.aligned) / release
 CACTO_D void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(dst_smem)), "r"(ncols)
