@@ -367,12 +367,12 @@ def main():
     # ---- roofline of the dominant kernel (K1 rollout over all candidates) ---------
     x0r = x0_dev
     for _ in range(2):
-        pipe.rollout_costs(x0r)
+        pipe.rollout_costs(x0r, keep_controls=True)
     evs = []
     for _ in range(5):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        pipe.rollout_costs(x0r)
+        pipe.rollout_costs(x0r, keep_controls=True)
         b.record()
         b.synchronize()
         evs.append(a.elapsed_time(b))
@@ -405,7 +405,7 @@ def main():
         "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (uniform workspace starts, Glorot-init networks, actor output layer x10)",
         "config": {"workload": f"{CONFIG_NAME}: {N} candidate starts/GPU -> T={T} rollout with cost, "
-                               f"sigma*|V-J| score, stable top-{keep_global} select, warm-start re-rollout",
+                               f"sigma*|V-J| score, stable top-{keep_global} select, kept warm starts (controls of the cost rollout)",
                    "candidates_per_gpu": N, "keep": keep_global, "hidden": [HIDDEN] * 3,
                    "horizon": T, "score": "std_x_gap", "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"shard-by-candidate x{world}"},
@@ -413,7 +413,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "kernel": kname, "kernel_ms": roll_ms, "flops_per_candidate_rollout": f_roll,
+                     "kernel": kname + ", emitting every candidate's controls (the kept warm starts)", "kernel_ms": roll_ms, "flops_per_candidate_rollout": f_roll,
                      "peak_source": peak_source,
                      "mma_passes": 3 if tc_path else None,
                      "fp32_ffma_peak": ffma_peak, "vs_ffma_peak": achieved / ffma_peak if ffma_peak else None},

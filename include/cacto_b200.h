@@ -154,6 +154,17 @@ int cacto_mlp_jacobian(const cacto_mlp_t* mlp, const void* xa, int64_t B, void* 
 int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
                   const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
                   void* U, void* X, void* step_costs, void* cost_to_go, void* stream);
+/* cacto_rollout with flags: CACTO_ROLLOUT_U_TIME_MAJOR writes U as [t_hor, m, N]
+ * (coalesced per step), so one cost rollout can also keep every candidate's
+ * controls and the kept warm starts are a column take (cacto_take_columns)
+ * instead of a second rollout (trainer.py:192-193 re-rolls the same starts). */
+enum { CACTO_ROLLOUT_U_TIME_MAJOR = 1 };
+int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
+                     const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
+                     int32_t flags, void* U, void* X, void* step_costs, void* cost_to_go, void* stream);
+/* dst[i, r] = src[r, idx[i]] for r < R, i < K: src [R, N] (dtype), dst [K, R] */
+int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int64_t N, const int64_t* idx, int64_t K,
+                       void* dst, void* stream);
 
 /* -- (a6, a8) BIC scores: std sigma(x0) (trainer.py:150-151), gap
  * |V(x0) - J(x0)| or sigma * gap (north_star).

@@ -72,6 +72,8 @@ _PCOST = ctypes.POINTER(CactoCost)
 _PBATCH = ctypes.POINTER(CactoBatch)
 _PI32 = ctypes.POINTER(ctypes.c_int32)
 
+ROLLOUT_U_TIME_MAJOR = 1   # CACTO_ROLLOUT_U_TIME_MAJOR
+
 # symbol -> (restype, argtypes); mirrors include/cacto_b200.h one to one
 SIGNATURES = {
     "cacto_abi_version": (ctypes.c_int, []),
@@ -81,6 +83,9 @@ SIGNATURES = {
     "cacto_mlp_forward": (ctypes.c_int, [_PMLP, _P, _I64, _P, _P]),
     "cacto_mlp_jacobian": (ctypes.c_int, [_PMLP, _P, _I64, _P, _P, _P]),
     "cacto_rollout": (ctypes.c_int, [_PSYS, _PCOST, _PMLP, _P, _P, _I32, _I64, _I32, _P, _P, _P, _P, _P]),
+    "cacto_rollout_ex": (ctypes.c_int, [_PSYS, _PCOST, _PMLP, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P, _P,
+                                         _P]),
+    "cacto_take_columns": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64, _P, _P]),
     "cacto_score": (ctypes.c_int, [_I32, _PMLP, _PMLP, _P, _P, _I64, _P, _P]),
     "cacto_select_workspace_bytes": (_SZ, [_I32, _I64, _I64]),
     "cacto_select_topk": (ctypes.c_int, [_I32, _P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P]),

@@ -10,6 +10,8 @@
 //               cost == Trajectory.cost (ilqr.py:76-78) term for term.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "net.cuh"
 #include "rollout.cuh"
 #include "systems.cuh"
@@ -90,7 +92,7 @@ rollout_kernel(const RolloutArgs<T> a) {
       for (int j = 0; j < m; ++j) u[j] = head_value(a.head, a.nc, j, US[j * S + s_own]);
       if (a.U) {
 #pragma unroll
-        for (int j = 0; j < m; ++j) a.U[(gi * a.t_stride + k) * m + j] = u[j];
+        for (int j = 0; j < m; ++j) a.U[a.u_at(gi, k, j, m)] = u[j];
       }
       T sc = T(0);
       if (a.has_cost) sc = stage_cost<SYS>(a.sys, a.cost, x, u);
@@ -197,6 +199,40 @@ static int system_dims_ok(const cacto_system_t* s) {
 extern "C" int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
                              const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
                              void* U, void* X, void* step_costs, void* cost_to_go, void* stream) {
+  return cacto_rollout_ex(sys, cost, actor, x0, t0, t0_scalar, N, t_hor, 0, U, X, step_costs, cost_to_go, stream);
+}
+
+namespace cacto {
+template <typename T>
+__global__ void take_columns_kernel(const T* __restrict__ src, int64_t R, int64_t N, const int64_t* __restrict__ idx,
+                                    int64_t K, T* dst) {
+  const int64_t total = R * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / R, rr = e - i * R;
+    dst[e] = src[rr * N + idx[i]];
+  }
+}
+}  // namespace cacto
+
+extern "C" int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int64_t N, const int64_t* idx, int64_t K,
+                                  void* dst, void* stream) {
+  if (R < 0 || N < 0 || K < 0 || (R * K > 0 && (!src || !idx || !dst)))
+    return set_error(CACTO_EVALUE, "take_columns: bad arguments");
+  if (R * K == 0) return CACTO_OK;
+  const int64_t total = R * K;
+  unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 16 * (int64_t)num_sms());
+  if (dtype == CACTO_F32)
+    take_columns_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)src, R, N, idx, K, (float*)dst);
+  else
+    take_columns_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)src, R, N, idx, K,
+                                                                         (double*)dst);
+  return check_launch("take_columns_kernel");
+}
+
+extern "C" int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
+                                const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
+                                int32_t flags, void* U, void* X, void* step_costs, void* cost_to_go, void* stream) {
+  if (flags & ~CACTO_ROLLOUT_U_TIME_MAJOR) return set_error(CACTO_EVALUE, "rollout: unknown flags %d", flags);
   if (!sys || !actor || !x0) return set_error(CACTO_EVALUE, "rollout: null argument");
   if (!system_dims_ok(sys)) return set_error(CACTO_EUNSUPPORTED, "rollout: unknown system kind %d / dims", sys->kind);
   if (N < 0) return set_error(CACTO_EVALUE, "rollout: N < 0");
@@ -219,6 +255,7 @@ extern "C" int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost
     a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
     a.params = (const float*)actor->params;
     a.x0 = x0; a.t0 = t0; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor; a.t_stride = stride;
+    a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : 0;
     a.U = (float*)U; a.X = (float*)X; a.SC = (float*)step_costs; a.C = (float*)cost_to_go;
     return dispatch_rollout(a, sys->kind, sh.hp, st);
   }
@@ -230,6 +267,7 @@ extern "C" int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost
   a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
   a.params = (const double*)actor->params;
   a.x0 = x0; a.t0 = t0; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor; a.t_stride = stride;
+  a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : 0;
   a.U = (double*)U; a.X = (double*)X; a.SC = (double*)step_costs; a.C = (double*)cost_to_go;
   return dispatch_rollout(a, sys->kind, sh.hp, st);
 }

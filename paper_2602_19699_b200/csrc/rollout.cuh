@@ -21,6 +21,10 @@ struct RolloutArgs {
   int64_t N;
   int t_hor;      // > 0 fixed horizon; 0 -> per-start t_max - t0
   int t_stride;   // row stride of the per-step outputs
+  int u_tmajor;   // U as [t_hor][m][N] (CACTO_ROLLOUT_U_TIME_MAJOR)
+  CACTO_D int64_t u_at(int64_t gi, int k, int j, int m) const {
+    return u_tmajor ? ((int64_t)k * m + j) * N + gi : (gi * t_stride + k) * m + j;
+  }
   T* U;
   T* X;
   T* SC;

@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
         for (int j = 0; j < m; ++j) u[j] = head_value(a.head, a.nc, j, o[j] * (1.f / WSCALE));
         if (a.U) {
 #pragma unroll
-          for (int j = 0; j < m; ++j) a.U[(gi * a.t_stride + k) * m + j] = u[j];
+          for (int j = 0; j < m; ++j) a.U[a.u_at(gi, k, j, m)] = u[j];
         }
         float sc = 0.f;
         if (a.has_cost) sc = stage_cost<SYS>(a.sys, a.cost, x, u);

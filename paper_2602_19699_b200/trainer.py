@@ -109,11 +109,22 @@ class BicPipeline:
         self.ws = SelectWorkspace()
         self.kernel_launches = 0
 
-    def rollout_costs(self, x0: torch.Tensor, t0: int = 0) -> torch.Tensor:
+    def rollout_costs(self, x0: torch.Tensor, t0: int = 0, keep_controls: bool = False) -> torch.Tensor:
+        """K1 cost-to-go of every candidate; with keep_controls the same launch
+        also writes every candidate's controls time-major into self.u_all
+        [T, m, N], from which the kept warm starts are taken (no second rollout)."""
         N = x0.shape[0]
-        cost = torch.empty(N, device=x0.device, dtype=torch_dtype(self.precision))
-        _lib.call("cacto_rollout", self.sysd, self.costd, self.actor.desc, x0.data_ptr(), None, t0, N,
-                  self.model.t_max - t0, None, None, None, cost.data_ptr(), _stream())
+        dt = torch_dtype(self.precision)
+        cost = torch.empty(N, device=x0.device, dtype=dt)
+        T = self.model.t_max - t0
+        U, flags = None, 0
+        if keep_controls:
+            shape = (T, self.model.m, N)
+            if getattr(self, "u_all", None) is None or tuple(self.u_all.shape) != shape or self.u_all.dtype != dt:
+                self.u_all = torch.empty(shape, device=x0.device, dtype=dt)
+            U, flags = self.u_all.data_ptr(), _lib.ROLLOUT_U_TIME_MAJOR
+        _lib.call("cacto_rollout_ex", self.sysd, self.costd, self.actor.desc, x0.data_ptr(), None, t0, N, T, flags,
+                  U, None, None, cost.data_ptr(), _stream())
         return cost
 
     def run(self, x0: torch.Tensor, keep: int, t0: int = 0, warm_starts: bool = True):
@@ -122,8 +133,9 @@ class BicPipeline:
         dt = torch_dtype(self.precision)
         launches = 0
         cost = None
+        reuse = warm_starts and keep > 0 and self.mode != "std"
         if self.mode != "std":
-            cost = self.rollout_costs(x0, t0)
+            cost = self.rollout_costs(x0, t0, keep_controls=reuse)
             launches += 1
         xa = torch.empty((N, n + 1), device=x0.device, dtype=dt)
         xa[:, :n] = x0
@@ -135,12 +147,18 @@ class BicPipeline:
         launches += 4 + max(0, int(np.ceil(np.log2(max(keep, 1) / 2048.0))))  # memset, select, sort, merges, emit
         out = {"order": order, "scores": top, "cost": cost}
         if warm_starts and keep > 0:
-            kept = x0.index_select(0, order)
-            launches += 1
             T = self.model.t_max - t0
             U = torch.empty((keep, T, self.model.m), device=x0.device, dtype=dt)
-            _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, keep, T,
-                      U.data_ptr(), None, None, None, _stream())
+            if reuse:
+                # the kept starts' controls from the cost rollout (same actor, start and t0:
+                # the trajectories trainer.py:192-193 would roll out again)
+                _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
+                          N, order.data_ptr(), keep, U.data_ptr(), _stream())
+            else:
+                kept = x0.index_select(0, order)
+                launches += 1
+                _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, keep, T,
+                          U.data_ptr(), None, None, None, _stream())
             launches += 1
             out["U"] = U
         if self.base_index:

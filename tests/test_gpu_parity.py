@@ -428,6 +428,27 @@ def test_bic_pipeline_vs_oracle_composition(mode, fp64):
     assert rel(U, U_ref) < 1e-9
 
 
+@pytest.mark.parametrize("mode", ["gap", "std_x_gap"])
+def test_bic_pipeline_warm_starts_equal_rerollout(mode, precision):
+    # gap modes keep every candidate's controls from the cost rollout (time-major)
+    # and take the kept columns: identical to rolling the kept starts out again
+    spec, fld = B_specs.config("dubins")
+    rng = np.random.default_rng(18)
+    c, h = B_specs.normalisation(spec)
+    d = spec.n + 1
+    actor = B_nets.init_mlp([d, 64, 64, 64, spec.m], rng, head="tanh", out_scale=spec.u_bound, in_center=c,
+                            in_half=h)
+    actor = actor.with_params([q * (5.0 if i == 6 else 1.0) for i, q in enumerate(actor.flat_params())])
+    critic = B_nets.init_mlp([d, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+    std = B_nets.init_mlp([d, 64, 64, 64, 1], rng, head="std", in_center=c, in_half=h)
+    x0 = torch.as_tensor(O_envs.sample_initial_states(spec, 40000, 3)).cuda()
+    pipe = B_trainer.BicPipeline(spec, fld, actor, critic, std, mode=mode)
+    out = pipe.run(x0, keep=4000)
+    kept = x0.index_select(0, out["order"]).cpu().numpy()
+    U = B_nets.actor_rollout_batch(actor, spec, kept, 0, None, None, emit=("U",))["U"]
+    np.testing.assert_array_equal(out["U"].cpu().numpy(), U)
+
+
 # ---- device-resident update loop (trainer.py:208-234) ------------------------------
 
 def _oracle_update_loop(spec, fld, nets0, rows, B, M, seed, k_s=1.0, tau=0.005, lrs=(5e-4, 1e-3, 1e-3)):
