@@ -162,6 +162,16 @@ enum { CACTO_ROLLOUT_U_TIME_MAJOR = 1 };
 int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
                      const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
                      int32_t flags, void* U, void* X, void* step_costs, void* cost_to_go, void* stream);
+/* K1 + K2 in one launch (gap modes): the rollout of every start with the cost,
+ * plus the BIC score of the same start from the std net / critic forwards on
+ * [x0, t0] (trainer.py:150-151 and the north_star gap score), written once the
+ * cost-to-go is known.  fp32 tensor-core path with std/critic of the actor's
+ * shape only; otherwise CACTO_EUNSUPPORTED before any launch (callers then use
+ * cacto_rollout_ex + cacto_score).  U optional (flags as cacto_rollout_ex). */
+int cacto_rollout_score(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
+                        int32_t mode, const cacto_mlp_t* std_net, const cacto_mlp_t* critic, const double* x0,
+                        int32_t t0_scalar, int64_t N, int32_t t_hor, int32_t flags, void* U, void* cost_to_go,
+                        void* scores, void* stream);
 /* dst[i, r] = src[r, idx[i]] for r < R, i < K: src [R, N] (dtype), dst [K, R] */
 int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int64_t N, const int64_t* idx, int64_t K,
                        void* dst, void* stream);

@@ -86,6 +86,8 @@ SIGNATURES = {
     "cacto_rollout_ex": (ctypes.c_int, [_PSYS, _PCOST, _PMLP, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P, _P,
                                          _P]),
     "cacto_take_columns": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64, _P, _P]),
+    "cacto_rollout_score": (ctypes.c_int, [_PSYS, _PCOST, _PMLP, _I32, _PMLP, _PMLP, _P, _I32, _I64, _I32, _I32,
+                                            _P, _P, _P, _P]),
     "cacto_score": (ctypes.c_int, [_I32, _PMLP, _PMLP, _P, _P, _I64, _P, _P]),
     "cacto_select_workspace_bytes": (_SZ, [_I32, _I64, _I64]),
     "cacto_select_topk": (ctypes.c_int, [_I32, _P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P]),

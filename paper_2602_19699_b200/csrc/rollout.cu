@@ -271,3 +271,83 @@ extern "C" int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* c
   a.U = (double*)U; a.X = (double*)X; a.SC = (double*)step_costs; a.C = (double*)cost_to_go;
   return dispatch_rollout(a, sys->kind, sh.hp, st);
 }
+
+// ---- K1 + K2 in one launch: rollout with the BIC scores of the same starts -------
+int validate_mlp(const cacto_mlp_t* m, const char* who);  // abi.cu
+
+static bool same_body(const cacto_mlp_t* a, const cacto_mlp_t* b) {
+  return b->dtype == a->dtype && b->hp == a->hp && b->n_layers == a->n_layers && b->activation == a->activation &&
+         b->sizes[0] == a->sizes[0];
+}
+
+extern "C" int cacto_rollout_score(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
+                                   int32_t mode, const cacto_mlp_t* std_net, const cacto_mlp_t* critic,
+                                   const double* x0, int32_t t0_scalar, int64_t N, int32_t t_hor, int32_t flags,
+                                   void* U, void* cost_to_go, void* scores, void* stream) {
+  if (mode < 0 || mode > 2) return set_error(CACTO_EVALUE, "rollout_score: unknown mode %d", mode);
+  if (!scores) return set_error(CACTO_EVALUE, "rollout_score: null scores");
+  if (flags & ~CACTO_ROLLOUT_U_TIME_MAJOR) return set_error(CACTO_EVALUE, "rollout_score: unknown flags %d", flags);
+  if (!sys || !actor || !x0) return set_error(CACTO_EVALUE, "rollout_score: null argument");
+  if (!system_dims_ok(sys)) return set_error(CACTO_EUNSUPPORTED, "rollout_score: unknown system kind %d", sys->kind);
+  const bool need_std = mode != CACTO_SCORE_GAP, need_crit = mode != CACTO_SCORE_STD;
+  int rc = validate_mlp(actor, "rollout_score(actor)");
+  if (rc) return rc;
+  if (need_std && (rc = validate_mlp(std_net, "rollout_score(std)"))) return rc;
+  if (need_crit && (rc = validate_mlp(critic, "rollout_score(critic)"))) return rc;
+  if (need_crit && !cost) return set_error(CACTO_EVALUE, "rollout_score: gap modes need the cost field");
+  if (actor->sizes[0] != sys->n + 1 || actor->sizes[actor->n_layers] != sys->m)
+    return set_error(CACTO_EVALUE, "rollout_score: actor dims do not match the system");
+  if (need_std && (std_net->sizes[std_net->n_layers] != 1 || std_net->head != CACTO_HEAD_STD))
+    return set_error(CACTO_EVALUE, "rollout_score: std net must be scalar with a std head");
+  if (need_crit && critic->sizes[critic->n_layers] != 1)
+    return set_error(CACTO_EVALUE, "rollout_score: critic must be scalar");
+  if (t_hor < 0 || t_hor > sys->t_max - t0_scalar)
+    return set_error(CACTO_EVALUE, "rollout of %d steps exceeds horizon from t=%d", t_hor, t0_scalar);
+  // fused only on the tensor-core path with nets of the actor's shape
+  NetShape sh = shape_of(*actor);
+  const bool tc_ok = actor->dtype == CACTO_F32 && rollout_tc_enabled() && sh.nh >= 1 && sh.nh <= 3 &&
+                     (sh.hp == 32 || sh.hp == 64) && sys->n + 1 <= 16 && sys->m <= 8 &&
+                     (!need_std || same_body(actor, std_net)) && (!need_crit || same_body(actor, critic));
+  if (!tc_ok) return set_error(CACTO_EUNSUPPORTED, "rollout_score: fused scoring needs the fp32 tensor-core path");
+  if (N == 0) return CACTO_OK;
+  RolloutArgs<float> a{};
+  a.sys = sys_dev<float>(*sys);
+  if (cost) a.cost = cost_dev<float>(*cost);
+  a.nc = net_const<float>(*actor);
+  a.has_cost = cost != nullptr;
+  a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
+  a.params = (const float*)actor->params;
+  a.x0 = x0; a.t0 = nullptr; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor;
+  a.t_stride = t_hor > 0 ? t_hor : sys->t_max;
+  a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : 0;
+  a.U = (float*)U; a.C = (float*)cost_to_go;
+  if (need_std) {
+    a.pre_kind[a.n_pre] = 0;
+    a.pre_params[a.n_pre] = (const float*)std_net->params;
+    a.pre_nc[a.n_pre] = net_const<float>(*std_net);
+    ++a.n_pre;
+  }
+  if (need_crit) {
+    a.pre_kind[a.n_pre] = 1;
+    a.pre_params[a.n_pre] = (const float*)critic->params;
+    a.pre_nc[a.n_pre] = net_const<float>(*critic);
+    ++a.n_pre;
+  }
+  a.score_mode = mode;
+  a.scores = (float*)scores;
+  cudaStream_t st = (cudaStream_t)stream;
+#define CACTO_RS_CASE(SYSK)                                                    \
+  case SYSK:                                                                   \
+    return sh.hp == 32 ? launch_rollout_tc<SYSK, 32>(a, st) : launch_rollout_tc<SYSK, 64>(a, st);
+  switch (sys->kind) {
+    CACTO_RS_CASE(CACTO_SYS_TOY1D)
+    CACTO_RS_CASE(CACTO_SYS_POINTMASS)
+    CACTO_RS_CASE(CACTO_SYS_DUBINS)
+    CACTO_RS_CASE(CACTO_SYS_MANIPULATOR3)
+    CACTO_RS_CASE(CACTO_SYS_ALIENGO_LIPM)
+    default:
+      break;
+  }
+#undef CACTO_RS_CASE
+  return set_error(CACTO_EUNSUPPORTED, "rollout_score: system kind %d", sys->kind);
+}

@@ -29,6 +29,15 @@ struct RolloutArgs {
   T* X;
   T* SC;
   T* C;
+  // fused BIC scoring (tensor-core path, trainer.py:150-151 + gap modes): forward
+  // passes of up to two scalar nets on [x0, t0] before the rollout, scores
+  // written when the cost-to-go is known
+  int n_pre;             // 0..2
+  int pre_kind[2];       // 0: std net (sigma head), 1: critic (linear head)
+  const T* pre_params[2];
+  NetConst<T> pre_nc[2];
+  int score_mode;        // CACTO_SCORE_*
+  T* scores;
 };
 
 // NumPy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) for

@@ -54,7 +54,8 @@ struct Plan {
   static constexpr uint32_t off_wh = off_w0 + 2 * W0;  // (hi, lo) x (nh - 1), nh <= 3
   static constexpr uint32_t off_wo = off_wh + 2 * 2 * WH;
   static constexpr uint32_t off_bias = off_wo + 2 * WO;  // fp32 [3][HP] + [NOUT], scaled
-  static constexpr uint32_t bytes = off_bias + (3 * HP + NOUT) * 4 + 1024;
+  // one network's slot (1024-aligned); slot 0 = actor, 1..2 = the scoring nets
+  static constexpr uint32_t SLOT = (off_bias + (3 * HP + NOUT) * 4 + 1023) / 1024 * 1024;
 };
 template <int HP, int NT>
 struct Tmem {
@@ -143,6 +144,28 @@ struct ActTC {
   }
 };
 
+// stage one network into its shared-memory slot: scaled hi/lo fp16 weights and
+// scaled biases (padded layout of include/cacto_b200.h)
+template <int HP, int IP, typename AF>
+CACTO_D void stage_net(unsigned char* slot, const float* P, int nh, int in, int out, int tid, int nthr) {
+  using PL = rtc::Plan<HP>;
+  const int64_t b0 = (int64_t)HP * IP;
+  float* bias = reinterpret_cast<float*>(slot + PL::off_bias);
+  rtc::stage_w(slot + PL::off_w0, slot + PL::off_w0 + PL::W0, P, HP, in, IP, AF::S, HP, rtc::KIN, tid, nthr);
+  rtc::stage_bias(bias, P, P + b0, HP, in, IP, AF::S, false, HP, tid, nthr);
+  int64_t off = b0 + HP;
+  for (int i = 1; i < nh; ++i) {
+    unsigned char* hi = slot + PL::off_wh + (uint32_t)(2 * (i - 1)) * PL::WH;
+    rtc::stage_w(hi, hi + PL::WH, P + off, HP, HP, HP, AF::S, HP, HP, tid, nthr);
+    rtc::stage_bias(bias + i * HP, P + off, P + off + (int64_t)HP * HP, HP, HP, HP, AF::S, AF::SHIFT, HP, tid, nthr);
+    off += (int64_t)HP * HP + HP;
+  }
+  rtc::stage_w(slot + PL::off_wo, slot + PL::off_wo + PL::WO, P + off, out, HP, HP, rtc::WSCALE, rtc::NOUT, HP, tid,
+               nthr);
+  rtc::stage_bias(bias + 3 * HP, P + off, P + off + (int64_t)out * HP, out, HP, HP, rtc::WSCALE, AF::SHIFT, rtc::NOUT,
+                  tid, nthr);
+}
+
 template <int SYS, int HP, int NT, int SPLIT, int ACT>
 __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(const RolloutArgs<float> a) {
   using namespace rtc;
@@ -167,26 +190,12 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nh = a.nh;
+  const int n_pre = a.n_pre;
 
-  // ---- weights -> shared memory (scaled, hi/lo fp16, SW128), scaled biases ---------
-  {
-    const float* P = a.params;
-    const int64_t b0 = (int64_t)HP * IP;
-    float* bias = reinterpret_cast<float*>(base + PL::off_bias);
-    stage_w(base + PL::off_w0, base + PL::off_w0 + PL::W0, P, HP, n + 1, IP, AF::S, HP, KIN, threadIdx.x, NTHR);
-    stage_bias(bias, P, P + b0, HP, n + 1, IP, AF::S, false, HP, threadIdx.x, NTHR);
-    int64_t off = b0 + HP;
-    for (int i = 1; i < nh; ++i) {
-      unsigned char* hi = base + PL::off_wh + (uint32_t)(2 * (i - 1)) * PL::WH;
-      stage_w(hi, hi + PL::WH, P + off, HP, HP, HP, AF::S, HP, HP, threadIdx.x, NTHR);
-      stage_bias(bias + i * HP, P + off, P + off + (int64_t)HP * HP, HP, HP, HP, AF::S, AF::SHIFT, HP, threadIdx.x,
-                 NTHR);
-      off += (int64_t)HP * HP + HP;
-    }
-    stage_w(base + PL::off_wo, base + PL::off_wo + PL::WO, P + off, m, HP, HP, WSCALE, NOUT, HP, threadIdx.x, NTHR);
-    stage_bias(bias + 3 * HP, P + off, P + off + (int64_t)m * HP, m, HP, HP, WSCALE, AF::SHIFT, NOUT, threadIdx.x,
-               NTHR);
-  }
+  // ---- networks -> shared-memory slots: 0 = actor, 1.. = the scoring nets --------
+  stage_net<HP, IP, AF>(base, a.params, nh, n + 1, m, threadIdx.x, NTHR);
+  for (int p = 0; p < n_pre; ++p)
+    stage_net<HP, IP, AF>(base + (p + 1) * PL::SLOT, a.pre_params[p], nh, n + 1, 1, threadIdx.x, NTHR);
   if (threadIdx.x == 0) {
     for (int t = 0; t < NT; ++t) {
       tc::mbar_init(&full_bar[t], WPT);
@@ -232,15 +241,18 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   }
   __syncthreads();
   const int kmax = s_kmax;
+  // passes: the scoring nets' forwards on [x0, t0], then the kmax actor steps
+  const int npass = n_pre + kmax;
 
   if (epi) {
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * TM::PER_TILE);
     const uint32_t t_d = lane_base, t_ahi = lane_base + HP, t_alo = lane_base + HP + HP / 2;
-    const uint32_t bias_s = sbase + PL::off_bias;
     const int c_base = part * COLS;
+    float sig = 0.f, val = 0.f;  // scoring nets' outputs
     uint32_t pd = 0;
-    // D[my columns] <- scaled bias of layer l (l == nh: the output layer, part 0)
-    auto preload_bias = [&](int l) {
+    // D[my columns] <- scaled bias of layer l of the net in `slot` (l == nh: output)
+    auto preload_bias = [&](int slot, int l) {
+      const uint32_t bias_s = sbase + (uint32_t)slot * PL::SLOT + PL::off_bias;
       if (l == nh) {
         if (part != 0) return;
         float b[16];
@@ -263,15 +275,17 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
         tc::tmem_st16(t_d + (uint32_t)(c_base + c0), b);
       }
     };
-    auto write_input = [&](int k) {
+    // normalised input row [x, t] of the net in `slot` (nets.py:126-129)
+    auto write_input = [&](int slot, int t_abs) {
       if (part != 0) return;
+      const NetConst<float>& nc = slot == 0 ? a.nc : a.pre_nc[slot - 1];
       float v[KIN];
 #pragma unroll
       for (int c = 0; c < KIN; ++c) v[c] = 0.f;
       if (owner) {
 #pragma unroll
-        for (int c = 0; c < n; ++c) v[c] = (x[c] - a.nc.in_center[c]) / a.nc.in_half[c];
-        v[n] = ((float)(t0 + k) - a.nc.in_center[n]) / a.nc.in_half[n];
+        for (int c = 0; c < n; ++c) v[c] = (x[c] - nc.in_center[c]) / nc.in_half[c];
+        v[n] = ((float)t_abs - nc.in_center[n]) / nc.in_half[n];
       }
       float hv[KIN / 2], lv[KIN / 2];
 #pragma unroll
@@ -295,12 +309,15 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       pd ^= 1;
       tc::tc_fence_after();
     };
-    if (kmax > 0) {
-      write_input(0);
-      preload_bias(0);
+    auto start_pass = [&](int P) {
+      const int slot = P < n_pre ? P + 1 : 0;
+      write_input(slot, P < n_pre ? t0 : t0 + (P - n_pre));
+      preload_bias(slot, 0);
       handoff();
-    }
-    for (int k = 0; k < kmax; ++k) {
+    };
+    if (npass > 0) start_pass(0);
+    for (int P = 0; P < npass; ++P) {
+      const int slot = P < n_pre ? P + 1 : 0;
       for (int l = 0; l < nh; ++l) {  // hidden layers
         wait_done();
 #pragma unroll
@@ -325,56 +342,63 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
             tc::tmem_st8(t_alo + ac, lv);
           }
         }
-        preload_bias(l + 1);
+        preload_bias(slot, l + 1);
         handoff();
       }
-      // output layer -> head, cost, dynamics
+      // output layer
       wait_done();
       float o[16];
       if (part == 0) tc::tmem_ld16_wait(t_d, o);
-      if (owner && k < T_i) {
-        float u[m];
+      if (slot != 0) {
+        // scoring net: sigma(x0) = sigma_min + softplus(o) or V(x0) = o
+        const float ov = o[0] * (1.f / WSCALE);
+        if (a.pre_kind[slot - 1] == 0) sig = head_value(CACTO_HEAD_STD, a.pre_nc[slot - 1], 0, ov);
+        else val = ov;
+      } else {
+        const int k = P - n_pre;
+        if (owner && k < T_i) {
+          float u[m];
 #pragma unroll
-        for (int j = 0; j < m; ++j) u[j] = head_value(a.head, a.nc, j, o[j] * (1.f / WSCALE));
-        if (a.U) {
+          for (int j = 0; j < m; ++j) u[j] = head_value(a.head, a.nc, j, o[j] * (1.f / WSCALE));
+          if (a.U) {
 #pragma unroll
-          for (int j = 0; j < m; ++j) a.U[a.u_at(gi, k, j, m)] = u[j];
-        }
-        float sc = 0.f;
-        if (a.has_cost) sc = stage_cost<SYS>(a.sys, a.cost, x, u);
-        acc.add(k, sc);
-        if (a.SC) a.SC[gi * (int64_t)(a.t_stride + 1) + k] = sc;
-        float xn[n];
-        step<SYS>(a.sys, x, u, xn);
+            for (int j = 0; j < m; ++j) a.U[a.u_at(gi, k, j, m)] = u[j];
+          }
+          float sc = 0.f;
+          if (a.has_cost) sc = stage_cost<SYS>(a.sys, a.cost, x, u);
+          acc.add(k, sc);
+          if (a.SC) a.SC[gi * (int64_t)(a.t_stride + 1) + k] = sc;
+          float xn[n];
+          step<SYS>(a.sys, x, u, xn);
 #pragma unroll
-        for (int c = 0; c < n; ++c) x[c] = xn[c];
-        if (a.X) {
+          for (int c = 0; c < n; ++c) x[c] = xn[c];
+          if (a.X) {
 #pragma unroll
-          for (int c = 0; c < n; ++c) a.X[(gi * (int64_t)(a.t_stride + 1) + k + 1) * n + c] = x[c];
+            for (int c = 0; c < n; ++c) a.X[(gi * (int64_t)(a.t_stride + 1) + k + 1) * n + c] = x[c];
+          }
         }
       }
-      if (k + 1 < kmax) {
-        write_input(k + 1);
-        preload_bias(0);
-        handoff();
-      }
+      if (P + 1 < npass) start_pass(P + 1);
     }
     if (owner) {
       const float term = a.has_cost ? terminal_cost<SYS>(a.sys, a.cost, x) : 0.f;
       acc.add(T_i, term);
       if (a.SC) a.SC[gi * (int64_t)(a.t_stride + 1) + T_i] = term;
       if (a.C) a.C[gi] = acc.res;
+      if (a.scores) {
+        const float gap = fabsf(val - acc.res);  // |V(x0) - J(x0)|
+        a.scores[gi] = a.score_mode == CACTO_SCORE_STD ? sig : (a.score_mode == CACTO_SCORE_GAP ? gap : sig * gap);
+      }
     }
   } else {
     // ---- MMA issuer (whole warp converged; elect.sync picks the issuing lane) ----------
     const uint32_t idesc_h = tc::idesc_f16(HP), idesc_o = tc::idesc_f16(NOUT);
     auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
-    const uint64_t w0h = desc(PL::off_w0), w0l = desc(PL::off_w0 + PL::W0);
-    const uint64_t woh = desc(PL::off_wo), wol = desc(PL::off_wo + PL::WO);
     uint32_t pf[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) pf[t] = 0;
-    for (int k = 0; k < kmax; ++k) {
+    for (int P = 0; P < npass; ++P) {
+      const uint32_t so = (uint32_t)(P < n_pre ? P + 1 : 0) * PL::SLOT;
       for (int l = 0; l <= nh; ++l) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
@@ -383,12 +407,12 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
           tc::tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(t * TM::PER_TILE), ahi = d + HP, alo = d + HP + HP / 2;
           if (l == 0) {
-            issue_layer<KIN / 16>(d, ahi, alo, w0h, w0l, idesc_h);
+            issue_layer<KIN / 16>(d, ahi, alo, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), idesc_h);
           } else if (l < nh) {
-            const uint32_t wo = PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;
+            const uint32_t wo = so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;
             issue_layer<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h);
           } else {
-            issue_layer<HP / 16>(d, ahi, alo, woh, wol, idesc_o);
+            issue_layer<HP / 16>(d, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), idesc_o);
           }
           tc::tc_commit_elect(&done_bar[t]);
           __syncwarp();
@@ -409,11 +433,12 @@ static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   constexpr int SPLIT = NT == 4 ? 1 : (NT == 2 ? (HP >= 32 ? 2 : 1) : (HP >= 64 ? 4 : HP / 16));
   auto kern = a.act == CACTO_ACT_ELU ? rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_ELU>
                                      : rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_TANH>;
-  if (!ensure_smem((const void*)kern, PL::bytes))
-    return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", PL::bytes);
+  const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + 1024;
+  if (!ensure_smem((const void*)kern, 3 * PL::SLOT + 1024))
+    return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", 3 * PL::SLOT + 1024);
   const int64_t per = (int64_t)NT * rtc::TILE;
   const int64_t blocks = (a.N + per - 1) / per;
-  kern<<<(unsigned)blocks, NT * SPLIT * 128 + 32, PL::bytes, st>>>(a);
+  kern<<<(unsigned)blocks, NT * SPLIT * 128 + 32, bytes, st>>>(a);
   return check_launch("rollout_tc_kernel");
 }
 

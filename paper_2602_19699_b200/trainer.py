@@ -127,6 +127,29 @@ class BicPipeline:
                   U, None, None, cost.data_ptr(), _stream())
         return cost
 
+    def _fused(self, x0: torch.Tensor, t0: int, keep_controls: bool):
+        """K1 + K2 in one launch (cacto_rollout_score); (None, None) when the
+        library reports the nets are not fusable."""
+        N = x0.shape[0]
+        dt = torch_dtype(self.precision)
+        cost = torch.empty(N, device=x0.device, dtype=dt)
+        scores = torch.empty(N, device=x0.device, dtype=dt)
+        T = self.model.t_max - t0
+        U, flags = None, 0
+        if keep_controls:
+            shape = (T, self.model.m, N)
+            if getattr(self, "u_all", None) is None or tuple(self.u_all.shape) != shape or self.u_all.dtype != dt:
+                self.u_all = torch.empty(shape, device=x0.device, dtype=dt)
+            U, flags = self.u_all.data_ptr(), _lib.ROLLOUT_U_TIME_MAJOR
+        rc = _lib.load().cacto_rollout_score(
+            self.sysd, self.costd, self.actor.desc, _lib.SCORE[self.mode], self.std.desc if self.std else None,
+            self.critic.desc if self.critic else None, x0.data_ptr(), t0, N, T, flags, U, cost.data_ptr(),
+            scores.data_ptr(), _stream())
+        if rc == _lib.EUNSUPPORTED:
+            return None, None
+        _lib.check(rc, "cacto_rollout_score")
+        return scores, cost
+
     def run(self, x0: torch.Tensor, keep: int, t0: int = 0, warm_starts: bool = True):
         """x0 float64 [N, n] on device -> dict(order, scores, U, cost)."""
         N, n = x0.shape
@@ -134,15 +157,18 @@ class BicPipeline:
         launches = 0
         cost = None
         reuse = warm_starts and keep > 0 and self.mode != "std"
+        scores = None
         if self.mode != "std":
-            cost = self.rollout_costs(x0, t0, keep_controls=reuse)
+            scores, cost = self._fused(x0, t0, reuse)
             launches += 1
-        xa = torch.empty((N, n + 1), device=x0.device, dtype=dt)
-        xa[:, :n] = x0
-        xa[:, n] = float(t0)
-        launches += 2  # torch copy + fill of the augmented view
-        scores = score_device(self.mode, xa, self.std, self.critic, cost)
-        launches += 1
+            if scores is None:  # not fusable (fp64 / SIMT path / differing net shapes)
+                cost = self.rollout_costs(x0, t0, keep_controls=reuse)
+        if scores is None:
+            xa = torch.empty((N, n + 1), device=x0.device, dtype=dt)
+            xa[:, :n] = x0
+            xa[:, n] = float(t0)
+            launches += 3  # torch copy + fill of the augmented view, K2 score
+            scores = score_device(self.mode, xa, self.std, self.critic, cost)
         order, top = select_topk_device(scores, keep, 0, self.ws)
         launches += 4 + max(0, int(np.ceil(np.log2(max(keep, 1) / 2048.0))))  # memset, select, sort, merges, emit
         out = {"order": order, "scores": top, "cost": cost}

@@ -15,6 +15,11 @@ KEYS = {
     "dram_write_bytes": ("dram__bytes_write.sum", 1),
     "fma_pipe_active_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1),
     "issue_active_pct": ("smsp__issue_active.avg.pct_of_peak_sustained_active", 1),
+    "tensor_pipe_active_pct": ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 1),
+    "xu_pipe_inst_pct": ("sm__inst_executed_pipe_xu.sum.pct_of_peak_sustained_active", 1),
+    "alu_pipe_inst_pct": ("sm__inst_executed_pipe_alu.sum.pct_of_peak_sustained_active", 1),
+    "fma_pipe_inst_pct": ("sm__inst_executed_pipe_fma.sum.pct_of_peak_sustained_active", 1),
+    "warp_instructions": ("smsp__inst_executed.sum", 1),
     "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1),
     "smem_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1),
     "smem_ld_bank_conflicts": ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", 1),

@@ -449,6 +449,34 @@ def test_bic_pipeline_warm_starts_equal_rerollout(mode, precision):
     np.testing.assert_array_equal(out["U"].cpu().numpy(), U)
 
 
+@pytest.mark.parametrize("mode", ["gap", "std_x_gap"])
+def test_fused_rollout_scores_match_separate_kernels(mode):
+    # cacto_rollout_score (K1 + K2 in one tensor-core launch) against the rollout
+    # followed by the separate score kernel on the same starts (fp32)
+    old = P.get_precision()
+    P.set_precision("fp32")
+    try:
+        spec, fld = B_specs.config("dubins")
+        rng = np.random.default_rng(19)
+        c, h = B_specs.normalisation(spec)
+        d = spec.n + 1
+        actor = B_nets.init_mlp([d, 64, 64, 64, spec.m], rng, head="tanh", out_scale=spec.u_bound, in_center=c,
+                                in_half=h)
+        critic = B_nets.init_mlp([d, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+        std = B_nets.init_mlp([d, 64, 64, 64, 1], rng, head="std", in_center=c, in_half=h)
+        x0 = torch.as_tensor(O_envs.sample_initial_states(spec, 20000, 5)).cuda()
+        pipe = B_trainer.BicPipeline(spec, fld, actor, critic, std, mode=mode)
+        scores, cost = pipe._fused(x0, 0, False)
+        assert scores is not None, "tensor-core fused path expected for fp32 3x64 nets"
+        cost2 = pipe.rollout_costs(x0, 0)
+        np.testing.assert_array_equal(cost.cpu().numpy(), cost2.cpu().numpy())
+        xa = torch.cat([x0.float(), torch.zeros(x0.shape[0], 1, device="cuda")], 1)
+        s2 = B_trainer.score_device(mode, xa, pipe.std, pipe.critic, cost2)
+        np.testing.assert_allclose(scores.cpu().numpy(), s2.cpu().numpy(), rtol=2e-5, atol=1e-5)
+    finally:
+        P.set_precision(old)
+
+
 # ---- device-resident update loop (trainer.py:208-234) ------------------------------
 
 def _oracle_update_loop(spec, fld, nets0, rows, B, M, seed, k_s=1.0, tau=0.005, lrs=(5e-4, 1e-3, 1e-3)):
