@@ -178,30 +178,30 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
   }
 }
 
-// bitonic sort of kSortChunk-pair chunks (pads with +inf pairs)
-__global__ void __launch_bounds__(kSelThreads) chunk_sort_kernel(Pair* data, int64_t M) {
+// bitonic sort of kSortChunk-pair chunks (pads with +inf pairs): one thread per
+// compare-exchange pair (kSortChunk / 2 threads), no idle lanes in any round
+constexpr int kSortThreads = kSortChunk / 2;
+__global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(Pair* data, int64_t M) {
   __shared__ Pair sh[kSortChunk];
   const int64_t base = (int64_t)blockIdx.x * kSortChunk;
-  for (int i = threadIdx.x; i < kSortChunk; i += kSelThreads)
+  for (int i = threadIdx.x; i < kSortChunk; i += kSortThreads)
     sh[i] = (base + i < M) ? data[base + i] : Pair{~0ull, 0x7fffffffffffffffll};
   __syncthreads();
+  const int p = threadIdx.x;
   for (int k = 2; k <= kSortChunk; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < kSortChunk; i += kSelThreads) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          bool up = (i & k) == 0;
-          Pair a = sh[i], b = sh[ixj];
-          if (pair_less(b, a) == up) {
-            sh[i] = b;
-            sh[ixj] = a;
-          }
-        }
+      const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));  // insert a 0 bit at log2(j)
+      const int ixj = i | j;
+      const bool up = (i & k) == 0;
+      const Pair a = sh[i], b = sh[ixj];
+      if (pair_less(b, a) == up) {
+        sh[i] = b;
+        sh[ixj] = a;
       }
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < kSortChunk; i += kSelThreads)
+  for (int i = threadIdx.x; i < kSortChunk; i += kSortThreads)
     if (base + i < M) data[base + i] = sh[i];
 }
 
@@ -252,7 +252,7 @@ static Pair* sort_pairs(Pair* a, Pair* b, int64_t M, int64_t first_width, cudaSt
   int64_t w = first_width;
   if (w <= 0) {
     int64_t chunks = (M + kSortChunk - 1) / kSortChunk;
-    if (chunks > 0) chunk_sort_kernel<<<(unsigned)chunks, kSelThreads, 0, st>>>(a, M);
+    if (chunks > 0) chunk_sort_kernel<<<(unsigned)chunks, kSortThreads, 0, st>>>(a, M);
     w = kSortChunk;
   }
   Pair* src = a;
