@@ -586,8 +586,6 @@ static int loss_grid(int64_t rows, int S) {
   return (int)(tiles < 1 ? 1 : (tiles < cap ? tiles : cap));
 }
 
-template <typename T>
-static constexpr int critic_S() { return sizeof(T) == 4 ? 64 : 32; }
 
 extern "C" size_t cacto_loss_workspace_bytes(const cacto_mlp_t* net, int64_t rows) {
   if (!net) return 0;
@@ -606,9 +604,13 @@ static void* scratch_of(const cacto_mlp_t* net, void* ws) {
   return (char*)ws + ((slots + 255) & ~(size_t)255);
 }
 
-template <typename T, int HP, int IP>
-static int launch_critic(const CriticArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
-  constexpr int S = critic_S<T>();
+// samples per CTA tile: 64 (fp32) once the batch gives every SM a tile, else 32 --
+// small minibatches (the M-cycle loop's B = 128) then spread over twice the CTAs
+// and each CTA's serial layer chain is half as long
+static bool small_batch(int64_t rows) { return rows < (int64_t)64 * num_sms(); }
+
+template <typename T, int HP, int IP, int S>
+static int launch_critic_s(const CriticArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
   size_t el = net_elems<T, HP, IP>(a.nh, 1) + 2 * (size_t)IP * S + (2 * (size_t)a.nh + 2) * HP * S + S +
               (size_t)CACTO_MAX_IN * S;
   size_t bytes = el * sizeof(T);
@@ -619,6 +621,14 @@ static int launch_critic(const CriticArgs<T>& a, int64_t rows, int* grid_out, cu
   kern<<<grid, kThreads, bytes, st>>>(a);
   *grid_out = grid;
   return check_launch("critic_kernel");
+}
+
+template <typename T, int HP, int IP>
+static int launch_critic(const CriticArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (!small_batch(rows)) return launch_critic_s<T, HP, IP, 64>(a, rows, grid_out, st);
+  }
+  return launch_critic_s<T, HP, IP, 32>(a, rows, grid_out, st);
 }
 
 template <typename T>
@@ -676,9 +686,8 @@ extern "C" int cacto_critic_loss(const cacto_mlp_t* critic, const cacto_mlp_t* t
   return critic_entry<double>(critic, target, batch, k_s, bootstrap, workspace, n_partials, st);
 }
 
-template <typename T, int HP, int IP, int KIND, int SYS>
-static int launch_vp(const VpArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
-  constexpr int S = critic_S<T>();
+template <typename T, int HP, int IP, int KIND, int SYS, int S>
+static int launch_vp_s(const VpArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
   size_t el = net_elems<T, HP, IP>(a.nh, a.out) + (size_t)IP * S + ((size_t)a.nh + 2) * HP * S +
               (size_t)CACTO_MAX_OUT * S + 4 * ((CACTO_MAX_OUT + 3) / 4) * S;
   size_t bytes = el * sizeof(T);
@@ -689,6 +698,14 @@ static int launch_vp(const VpArgs<T>& a, int64_t rows, int* grid_out, cudaStream
   kern<<<grid, kThreads, bytes, st>>>(a);
   *grid_out = grid;
   return check_launch("vp_kernel");
+}
+
+template <typename T, int HP, int IP, int KIND, int SYS>
+static int launch_vp(const VpArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (!small_batch(rows)) return launch_vp_s<T, HP, IP, KIND, SYS, 64>(a, rows, grid_out, st);
+  }
+  return launch_vp_s<T, HP, IP, KIND, SYS, 32>(a, rows, grid_out, st);
 }
 
 #define CACTO_VP_DISPATCH(T, KIND, SYS, hp, ip, a, rows, grid, st)                   \
@@ -716,9 +733,7 @@ static int std_entry(const cacto_mlp_t* sn, const cacto_mlp_t* cn, const cacto_b
   a.inv_denom = T(1) / (T)(b->denom > 0 ? b->denom : b->rows);
   a.err = err;
   a.ws = (T*)ws;
-  int grid = 0;
-  CACTO_VP_DISPATCH(T, VP_STD, 0, sh.hp, sh.ip, a, b->rows, &grid, st);
-  (void)n_partials;
+  CACTO_VP_DISPATCH(T, VP_STD, 0, sh.hp, sh.ip, a, b->rows, n_partials, st);
   return set_error(CACTO_EUNSUPPORTED, "std_loss: hidden %d / input %d not built", sh.hp, sh.in);
 }
 
@@ -738,12 +753,6 @@ extern "C" int cacto_std_loss(const cacto_mlp_t* std_net, const cacto_mlp_t* cri
     *n_partials = 1;
     return wide_std_loss(std_net, critic, batch, workspace, workspace_bytes, st);
   }
-  int grid = 0;
-  NetShape sh = shape_of(*std_net);
-  int S = std_net->dtype == CACTO_F32 ? 64 : 32;
-  grid = loss_grid(batch->rows, S);
-  *n_partials = grid;
-  (void)sh;
   if (std_net->dtype == CACTO_F32) return std_entry<float>(std_net, critic, batch, workspace, n_partials, st);
   return std_entry<double>(std_net, critic, batch, workspace, n_partials, st);
 }
@@ -807,9 +816,7 @@ static int actor_sys(const cacto_mlp_t* an, const cacto_mlp_t* cn, const cacto_s
   a.vn = vn;
   a.gn = gn;
   a.ws = (T*)ws;
-  int grid = 0;
-  *n_partials = loss_grid(R, critic_S<T>());
-  CACTO_VP_DISPATCH(T, VP_ACTOR, SYS, sh.hp, sh.ip, a, R, &grid, st);
+  CACTO_VP_DISPATCH(T, VP_ACTOR, SYS, sh.hp, sh.ip, a, R, n_partials, st);
   return set_error(CACTO_EUNSUPPORTED, "actor_loss: hidden %d / input %d not built", sh.hp, sh.in);
 }
 
