@@ -608,6 +608,7 @@ static void* scratch_of(const cacto_mlp_t* net, void* ws) {
 // small minibatches (the M-cycle loop's B = 128) then spread over twice the CTAs
 // and each CTA's serial layer chain is half as long
 static bool small_batch(int64_t rows) { return rows < (int64_t)64 * num_sms(); }
+static bool tiny_batch(int64_t rows) { return rows <= (int64_t)16 * num_sms(); }
 
 template <typename T, int HP, int IP, int S>
 static int launch_critic_s(const CriticArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
@@ -627,6 +628,9 @@ template <typename T, int HP, int IP>
 static int launch_critic(const CriticArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
     if (!small_batch(rows)) return launch_critic_s<T, HP, IP, 64>(a, rows, grid_out, st);
+    if constexpr (HP == 64) {
+      if (tiny_batch(rows)) return launch_critic_s<T, HP, IP, 16>(a, rows, grid_out, st);
+    }
   }
   return launch_critic_s<T, HP, IP, 32>(a, rows, grid_out, st);
 }
@@ -704,6 +708,9 @@ template <typename T, int HP, int IP, int KIND, int SYS>
 static int launch_vp(const VpArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
     if (!small_batch(rows)) return launch_vp_s<T, HP, IP, KIND, SYS, 64>(a, rows, grid_out, st);
+    if constexpr (HP == 64) {
+      if (tiny_batch(rows)) return launch_vp_s<T, HP, IP, KIND, SYS, 16>(a, rows, grid_out, st);
+    }
   }
   return launch_vp_s<T, HP, IP, KIND, SYS, 32>(a, rows, grid_out, st);
 }
