@@ -2,12 +2,28 @@
 // per-sample input Jacobian (nets.mlp_input_gradient / value_and_state_grad,
 // nets.py:176-206) and the fused BIC score (trainer.py:150-151 std mode;
 // north_star gap mode |V(x0) - J(x0)|).
+#include <type_traits>
+
 #include "net.cuh"
 
 namespace cacto {
 
 template <typename T>
-constexpr int fwd_S() { return sizeof(T) == 4 ? 64 : 32; }  // samples per tile
+constexpr int fwd_S() { return sizeof(T) == 4 ? 64 : 32; }  // samples per tile (large batches)
+
+// samples per tile for a batch of `rows`: fp32 uses 64 once every SM gets a tile,
+// else 32 (16 for tiny batches at hidden 64) so small minibatches spread over
+// more CTAs; fp64 always 32
+template <typename T, int HP, typename F>
+static int with_tile(int64_t rows, F f) {
+  if constexpr (sizeof(T) == 4) {
+    if (rows >= (int64_t)64 * num_sms()) return f(std::integral_constant<int, 64>());
+    if constexpr (HP == 64) {
+      if (rows <= (int64_t)16 * num_sms()) return f(std::integral_constant<int, 16>());
+    }
+  }
+  return f(std::integral_constant<int, 32>());
+}
 
 template <typename T>
 struct FwdArgs {
@@ -20,9 +36,8 @@ struct FwdArgs {
   T* out_jac;  // [B][out][in] (jacobian kernel)
 };
 
-template <typename T, int HP, int IP>
+template <typename T, int HP, int IP, int S>
 __global__ void __launch_bounds__(kThreads) mlp_forward_kernel(const FwdArgs<T> a) {
-  constexpr int S = fwd_S<T>();
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -47,9 +62,8 @@ __global__ void __launch_bounds__(kThreads) mlp_forward_kernel(const FwdArgs<T> 
   }
 }
 
-template <typename T, int HP, int IP>
+template <typename T, int HP, int IP, int S>
 __global__ void __launch_bounds__(kThreads) mlp_jacobian_kernel(const FwdArgs<T> a) {
-  constexpr int S = fwd_S<T>();
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -154,11 +168,11 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreArgs<T> a) {
 
 template <typename T, int HP, int IP, typename K>
 static int launch_tiles(K kern, size_t smem_elems, int64_t rows, cudaStream_t st, const char* name,
-                        const void* args_ptr) {
+                        const void* args_ptr, int S = fwd_S<T>()) {
   size_t bytes = smem_elems * sizeof(T);
   if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_ECUDA, "%s: %zu B of shared memory not available", name, bytes);
-  int64_t tiles = (rows + fwd_S<T>() - 1) / fwd_S<T>();
+  int64_t tiles = (rows + S - 1) / S;
   int64_t grid = tiles < 4 * num_sms() ? tiles : 4 * num_sms();
   if (grid < 1) grid = 1;
   (void)args_ptr;
@@ -167,23 +181,25 @@ static int launch_tiles(K kern, size_t smem_elems, int64_t rows, cudaStream_t st
 
 template <typename T, int HP, int IP>
 static int run_forward(const FwdArgs<T>& a, bool jac, cudaStream_t st) {
-  constexpr int S = fwd_S<T>();
-  size_t net_el = net_elems<T, HP, IP>(a.nh, a.out);
-  size_t el = net_el + (size_t)IP * S + 2 * (size_t)HP * S;
-  if (jac) el += (size_t)(a.nh > 0 ? a.nh : 1) * HP * S + (size_t)a.out * S;
-  int grid;
-  if (jac) {
-    auto kern = mlp_jacobian_kernel<T, HP, IP>;
-    grid = launch_tiles<T, HP, IP>(kern, el, a.B, st, "mlp_jacobian", &a);
+  return with_tile<T, HP>(a.B, [&](auto s_) {
+    constexpr int S = decltype(s_)::value;
+    size_t net_el = net_elems<T, HP, IP>(a.nh, a.out);
+    size_t el = net_el + (size_t)IP * S + 2 * (size_t)HP * S;
+    if (jac) el += (size_t)(a.nh > 0 ? a.nh : 1) * HP * S + (size_t)a.out * S;
+    int grid;
+    if (jac) {
+      auto kern = mlp_jacobian_kernel<T, HP, IP, S>;
+      grid = launch_tiles<T, HP, IP>(kern, el, a.B, st, "mlp_jacobian", &a, S);
+      if (grid < 0) return grid;
+      kern<<<grid, kThreads, el * sizeof(T), st>>>(a);
+      return check_launch("mlp_jacobian_kernel");
+    }
+    auto kern = mlp_forward_kernel<T, HP, IP, S>;
+    grid = launch_tiles<T, HP, IP>(kern, el, a.B, st, "mlp_forward", &a, S);
     if (grid < 0) return grid;
     kern<<<grid, kThreads, el * sizeof(T), st>>>(a);
-    return check_launch("mlp_jacobian_kernel");
-  }
-  auto kern = mlp_forward_kernel<T, HP, IP>;
-  grid = launch_tiles<T, HP, IP>(kern, el, a.B, st, "mlp_forward", &a);
-  if (grid < 0) return grid;
-  kern<<<grid, kThreads, el * sizeof(T), st>>>(a);
-  return check_launch("mlp_forward_kernel");
+    return check_launch("mlp_forward_kernel");
+  });
 }
 
 template <typename T, int HP, int IP>
@@ -337,9 +353,8 @@ struct RowsArgs {
   T* out;
 };
 
-template <typename T, int HP, int IP>
+template <typename T, int HP, int IP, int S>
 __global__ void __launch_bounds__(kThreads) rows_forward_kernel(const RowsArgs<T> a) {
-  constexpr int S = fwd_S<T>();
   using TL = Tile<T, S, HP>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -375,13 +390,15 @@ __global__ void __launch_bounds__(kThreads) rows_forward_kernel(const RowsArgs<T
 
 template <typename T, int HP, int IP>
 static int run_rows(const RowsArgs<T>& a, cudaStream_t st) {
-  constexpr int S = fwd_S<T>();
-  size_t el = net_elems<T, HP, IP>(a.nh, 1) + (size_t)IP * S + 2 * (size_t)HP * S;
-  auto kern = rows_forward_kernel<T, HP, IP>;
-  int grid = launch_tiles<T, HP, IP>(kern, el, a.rows, st, "rows_forward", &a);
-  if (grid < 0) return grid;
-  kern<<<grid, kThreads, el * sizeof(T), st>>>(a);
-  return check_launch("rows_forward_kernel");
+  return with_tile<T, HP>(a.rows, [&](auto s_) {
+    constexpr int S = decltype(s_)::value;
+    size_t el = net_elems<T, HP, IP>(a.nh, 1) + (size_t)IP * S + 2 * (size_t)HP * S;
+    auto kern = rows_forward_kernel<T, HP, IP, S>;
+    int grid = launch_tiles<T, HP, IP>(kern, el, a.rows, st, "rows_forward", &a, S);
+    if (grid < 0) return grid;
+    kern<<<grid, kThreads, el * sizeof(T), st>>>(a);
+    return check_launch("rows_forward_kernel");
+  });
 }
 
 template <typename T>
