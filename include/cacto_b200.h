@@ -216,7 +216,8 @@ int cacto_ring_push(const cacto_batch_t* src, void* ring_xa, void* ring_u, void*
  * parameter layout of the differentiated network; the loss is a scalar.
  *   critic: nets.critic_loss, nets.py:233-290 (target may be NULL)
  *   actor:  nets.actor_loss, nets.py:293-334 (rows with t >= t_max skipped;
- *           live-row count written to `live_rows` [1] int64 device)
+ *           the loss divides by the live-row count: `live_rows` [1] int64 device
+ *           from cacto_count_live, or NULL to count inside the loss launch)
  *   std:    nets.std_critic_loss, nets.py:337-353
  * Wide networks (hp > 64) are differentiated layer by layer on the tensor
  * cores and always report n_partials = 1.  For cacto_actor_loss pass

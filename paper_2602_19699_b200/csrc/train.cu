@@ -347,6 +347,7 @@ struct VpArgs {
   Offs off;
   BatchDev<T> b;
   const int64_t* live_rows;  // device count (actor) or null -> inv_denom
+  int count_live;            // actor: count the live rows in-kernel (live_rows == null)
   T inv_denom;
   // std loss
   const T* err;  // [rows] v_bar - V(xa)
@@ -387,7 +388,18 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
   const int64_t P_total = a.off.total;
   T* slot = a.ws + (int64_t)blockIdx.x * (P_total + 1);
   zero_slot(slot, P_total + 1);
-  const T inv_denom = a.live_rows ? T(1) / (T)(*a.live_rows) : a.inv_denom;
+  T inv_denom = a.live_rows ? T(1) / (T)(*a.live_rows) : a.inv_denom;
+  if (a.count_live) {  // rows with t < t_max (nets.py:310-312), counted by every CTA
+    __shared__ unsigned int live_acc;
+    if (threadIdx.x == 0) live_acc = 0;
+    __syncthreads();
+    unsigned int c = 0;
+    for (int64_t b = threadIdx.x; b < a.b.rows; b += kThreads)
+      c += a.b.xa[a.b.row(b) * (a.b.n + 1) + a.b.n] < (T)a.b.t_max ? 1u : 0u;
+    atomicAdd(&live_acc, c);
+    __syncthreads();
+    inv_denom = T(1) / (T)live_acc;
+  }
 
   const TL tl;
   const int nh = a.nh, L1 = nh, out = a.out, n = a.b.n;
@@ -764,9 +776,8 @@ extern "C" int cacto_std_loss(const cacto_mlp_t* std_net, const cacto_mlp_t* cri
   return std_entry<double>(std_net, critic, batch, workspace, n_partials, st);
 }
 
-template <typename T, int HP, int IP, int SYS>
-static int launch_prep(const PrepArgs<T>& a, cudaStream_t st) {
-  constexpr int S = 64;
+template <typename T, int HP, int IP, int SYS, int S>
+static int launch_prep_s(const PrepArgs<T>& a, cudaStream_t st) {
   size_t el = net_elems<T, HP, IP>(a.nh, a.out) + (size_t)IP * S + 2 * (size_t)HP * S + (size_t)CACTO_MAX_OUT * S;
   size_t bytes = el * sizeof(T);
   auto kern = actor_prep_kernel<T, HP, IP, S, SYS>;
@@ -776,6 +787,15 @@ static int launch_prep(const PrepArgs<T>& a, cudaStream_t st) {
   int grid = (int)(tiles < 2 * num_sms() ? tiles : 2 * num_sms());
   kern<<<grid, kThreads, bytes, st>>>(a);
   return check_launch("actor_prep_kernel");
+}
+
+template <typename T, int HP, int IP, int SYS>
+static int launch_prep(const PrepArgs<T>& a, cudaStream_t st) {
+  if (!small_batch(a.b.rows)) return launch_prep_s<T, HP, IP, SYS, 64>(a, st);
+  if constexpr (HP == 64) {
+    if (tiny_batch(a.b.rows)) return launch_prep_s<T, HP, IP, SYS, 16>(a, st);
+  }
+  return launch_prep_s<T, HP, IP, SYS, 32>(a, st);
 }
 
 template <typename T, int SYS>
@@ -816,6 +836,7 @@ static int actor_sys(const cacto_mlp_t* an, const cacto_mlp_t* cn, const cacto_s
   a.off = offs_of(*an);
   a.b = pa.b;
   a.live_rows = live;
+  a.count_live = live == nullptr;
   a.sys = pa.sys;
   a.cost = pa.cost;
   a.xn = xn;
@@ -848,7 +869,7 @@ extern "C" int cacto_actor_loss(const cacto_mlp_t* actor, const cacto_mlp_t* cri
   if (rc) return rc;
   rc = validate_mlp(critic, "actor_loss(critic)");
   if (rc) return rc;
-  if (!sys || !cost || !batch || !live_rows) return set_error(CACTO_EVALUE, "actor_loss: null argument");
+  if (!sys || !cost || !batch) return set_error(CACTO_EVALUE, "actor_loss: null argument");
   if (batch->rows <= 0) return set_error(CACTO_EVALUE, "empty batch");
   if (actor->sizes[0] != sys->n + 1 || actor->sizes[actor->n_layers] != sys->m || critic->sizes[0] != sys->n + 1)
     return set_error(CACTO_EVALUE, "actor_loss: dims do not match the system");

@@ -714,10 +714,16 @@ static int wide_actor_sys(const cacto_mlp_t* am, const cacto_mlp_t* cm, const ca
   float* GN = ar.f((size_t)B * (nn + 1));
   float* DEL = ar.f((size_t)B * 8);
   float* lossp = ar.f(1024);
+  int64_t* live_own = live ? nullptr : reinterpret_cast<int64_t*>(ar.f(2));  // live == null: count here
   size_t cws = ar.left;  // the rest for the critic Jacobian
   void* cwsp = ar.p;
   if (!ar.ok) return set_error(CACTO_EVALUE, "wide actor: workspace too small");
   cudaMemsetAsync(slot, 0, ((size_t)w.lo.total + 1) * 4, st);
+  if (live_own) {
+    int rc0 = cacto_count_live(bt, live_own, st);
+    if (rc0) return rc0;
+    live = live_own;
+  }
   RowSrc xs = batch_src(bt, bt->xa, nn + 1);
   fill_input(c, w, a.X0, B, xs);
   int rc = forward(c, w, a, B);

@@ -118,10 +118,10 @@ class UpdateEngine:
         _lib.call("cacto_critic_loss", self.critic.dn.desc, tgt.desc if tgt else None, bd, self.k_s,
                   int(self.bootstrap), self.ws_c.data_ptr(), self.ws_c.numel(), npart, st)
         self._adam(self.critic, self.ws_c, npart.value, 0, target=self.target, loss=self.closs)  # trainer.py:216-220
-        _lib.call("cacto_count_live", bd, self.live.data_ptr(), st)
         npa = ctypes.c_int32(0)
+        # live rows (nets.py:310-312) counted inside the actor-loss launch (live_rows = NULL)
         _lib.call("cacto_actor_loss", self.actor.dn.desc, self.critic.dn.desc, self.sysd, self.costd, bd,
-                  self.live.data_ptr(), self.ws_a.data_ptr(), self.ws_a.numel(), npa, st)
+                  None, self.ws_a.data_ptr(), self.ws_a.numel(), npa, st)
         self._adam(self.actor, self.ws_a, npa.value, 0, loss=self.aloss)                        # trainer.py:223-225
         _lib.call("cacto_counter_tick", self.cnt[0:1].data_ptr(), st)
 
