@@ -423,9 +423,10 @@ def main():
     }
 
     # ---- secondary: critic Sobolev samples/s (manipulator dims, B = 65536) ----------
-    if not args.no_secondary and rank == 0:
+    if not args.no_secondary:
         try:
-            line["secondary"] = critic_bench(torch, P, stream)
+            line["secondary"] = critic_bench(torch, P, stream, world=world, rank=rank,
+                                             dist=dist if world > 1 else None)
         except Exception as e:  # keep the primary line alive
             line["secondary"] = {"error": str(e)[:200]}
 
@@ -443,12 +444,18 @@ def main():
         dist.destroy_process_group()
 
 
-def critic_bench(torch, P, stream, B=65536):
-    """One Sobolev critic update (fused loss + fold/Adam/Polyak) per step."""
+def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
+    """One Sobolev critic update per step (fused gather + target forward + Sobolev
+    loss with double backprop + fold + Adam + Polyak), data-parallel over ranks:
+    every rank draws the same global index stream and takes its B-row slice (weak
+    scaling: B per GPU), losses divide by the global batch, and at world > 1 the
+    folded gradient (+ loss) is summed with one NCCL all-reduce before Adam
+    (north_star: "critic/actor minibatches are data-parallel with an NCCL gradient
+    allreduce").  Device-timed, max over ranks."""
     import ctypes
     from paper_2602_19699_b200 import _lib, specs
     from paper_2602_19699_b200.device import DeviceNet
-    from paper_2602_19699_b200.buffer import ReplayBuffer
+    from paper_2602_19699_b200.buffer import ReplayBuffer, SampleBatch
     spec, _ = specs.config("manipulator3")
     actor, critic, std = make_nets(spec)
     net = DeviceNet(critic)
@@ -462,28 +469,41 @@ def critic_bench(torch, P, stream, B=65536):
                          rng.integers(0, spec.t_max, (rows, 1))], axis=1)
     xk = np.concatenate([rng.uniform(size=(rows, spec.n)) * (hi - lo) + lo,
                          rng.integers(1, spec.t_max + 1, (rows, 1))], axis=1)
-    from paper_2602_19699_b200.buffer import SampleBatch
     buf.push_many(SampleBatch(xa, rng.normal(size=(rows, spec.m)), rng.normal(size=rows),
                               rng.normal(size=(rows, spec.n)), xk, spec.t_max))
-    idx = torch.as_tensor(rng.integers(0, rows, B)).cuda()
+    idx_all = rng.integers(0, rows, B * world)           # the global stream, same on every rank
+    idx = torch.as_tensor(idx_all[rank * B:(rank + 1) * B]).cuda()
     desc = buf.ring_desc(idx, rows=B)
+    desc.denom = B * world                                 # mean over the global batch
     nbytes = _lib.load().cacto_loss_workspace_bytes(net.desc, B)
     ws = torch.empty(nbytes, device="cuda", dtype=torch.uint8)
     m = torch.zeros_like(net.params)
     v = torch.zeros_like(net.params)
+    g = torch.empty(net.count + 1, device="cuda", dtype=net.params.dtype)  # grads + loss, one all-reduce
     npart = ctypes.c_int32(0)
     step_no = [0]
 
     def one():
         _lib.call("cacto_critic_loss", net.desc, tgt.desc, desc, 1.0, 1, ws.data_ptr(), nbytes, npart, stream)
-        _lib.call("cacto_reduce_adam", net.desc.dtype, ws.data_ptr(), npart.value, net.count, net.params.data_ptr(),
-                  m.data_ptr(), v.data_ptr(), step_no[0], 1e-3, 0.9, 0.999, 1e-8, tgt.params.data_ptr(), 0.005,
-                  None, None, stream)
+        if world == 1:
+            _lib.call("cacto_reduce_adam", net.desc.dtype, ws.data_ptr(), npart.value, net.count,
+                      net.params.data_ptr(), m.data_ptr(), v.data_ptr(), step_no[0], 1e-3, 0.9, 0.999, 1e-8,
+                      tgt.params.data_ptr(), 0.005, None, None, stream)
+        else:
+            _lib.call("cacto_reduce_grads", net.desc.dtype, ws.data_ptr(), npart.value, net.count, g.data_ptr(),
+                      g[net.count:].data_ptr(), stream)
+            dist.all_reduce(g)
+            _lib.call("cacto_adam_step", net.desc.dtype, net.params.data_ptr(), m.data_ptr(), v.data_ptr(),
+                      g.data_ptr(), net.count, step_no[0], 1e-3, 0.9, 0.999, 1e-8, stream)
+            _lib.call("cacto_polyak", net.desc.dtype, tgt.params.data_ptr(), net.params.data_ptr(), net.count, 0.005,
+                      stream)
         step_no[0] += 1
 
     for _ in range(3):
         one()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     K = 10
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
@@ -492,12 +512,19 @@ def critic_bench(torch, P, stream, B=65536):
     b.record()
     b.synchronize()
     ms = a.elapsed_time(b) / K
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     H, d = HIDDEN, spec.n + 1
     f = 28 * H * H + 14 * d * H + 8 * H
-    return {"metric": "critic Sobolev samples/sec", "value": B / (ms * 1e-3), "unit": "samples/s",
-            "batch": B, "hidden": [H] * 3, "ms_per_update": ms, "system": "manipulator3 (d=7)",
-            "achieved_tflops": f * B / (ms * 1e-3) / 1e12, "flops_per_sample": f,
-            "includes": "fused gather + target forward + Sobolev fwd/double-backprop + fold + Adam + Polyak"}
+    return {"metric": "critic Sobolev samples/sec", "value": B * world / (ms * 1e-3), "unit": "samples/s",
+            "batch_per_gpu": B, "global_batch": B * world, "n_gpus": world, "hidden": [H] * 3,
+            "ms_per_update": ms, "system": "manipulator3 (d=7)", "scaling": "weak",
+            "achieved_tflops": f * B * world / (ms * 1e-3) / 1e12, "flops_per_sample": f,
+            "includes": "fused gather + target forward + Sobolev fwd/double-backprop + fold + "
+                        + ("Adam + Polyak" if world == 1 else "NCCL all-reduce of the gradient + Adam + Polyak"),
+            "sweep": "profiles/critic_sweep.py (batch 4k-1M x hidden 64-512, 1 GPU)"}
 
 
 if __name__ == "__main__":
