@@ -384,8 +384,9 @@ def main():
         # K1 runs its policy layers on tcgen05 (kind::tf32, 3 MMA passes for fp32
         # accuracy): the roofline is the TF32 tensor pipe
         peak, bound = TF32_DENSE_TFLOPS, "tensor"
-        peak_source = ("B200_PROFILING.md fallback: tf32 dense 1.1 PFLOP/s (MEASURED_PEAKS.json has no tf32 "
-                       "entry); algorithmic flops count each product once, the 3xTF32 split issues 3x")
+        peak_source = ("B200_PROFILING.md fallback: tf32 dense 1.1 PFLOP/s, the fp32-class tensor format "
+                       "(MEASURED_PEAKS.json has no tf32 entry); algorithmic flops count each product once, the "
+                       "3xFP16 split issues 3x the MMAs at twice tf32's per-K rate")
         kname = "rollout_tc_kernel (K1 on tcgen05, cost-only over all candidates)"
     else:
         peak, bound = ffma_peak, "fp32_simt"
@@ -416,6 +417,10 @@ def main():
                      "kernel": kname + ", emitting every candidate's controls (the kept warm starts)", "kernel_ms": roll_ms, "flops_per_candidate_rollout": f_roll,
                      "peak_source": peak_source,
                      "mma_passes": 3 if tc_path else None,
+                     "mma_issued_tflops": 3 * achieved if tc_path else None,
+                     "mma_kind": "tcgen05 kind::f16, 3xFP16 split (fp16 dense peak 2250 TFLOP/s)" if tc_path else None,
+                     "binding_resource": ("CUDA-core epilogue issue (ncu: issue active ~71 %, tensor pipe ~25 %; "
+                                          "profiles/r01_ncu_rollout_tc.json)") if tc_path else None,
                      "fp32_ffma_peak": ffma_peak, "vs_ffma_peak": achieved / ffma_peak if ffma_peak else None},
         "clocks": clk,
         "flops_per_candidate": f_cand,

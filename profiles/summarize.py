@@ -76,12 +76,15 @@ def full(rep, out):
     print(json.dumps(res, indent=1)[:3000])
 
 
-def launches(path, out):
+def launches(path, out, exclude=None):
+    import re
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h, rows = rows[0], rows[1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     agg = collections.OrderedDict()
     for r in rows:
+        if exclude and re.search(exclude, r[ki]):
+            continue
         v = _num(r[vi])
         scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}.get(r[ui], 1e-6)
         a = agg.setdefault(r[ki], [0, 0.0])
@@ -91,13 +94,15 @@ def launches(path, out):
     res = [{"kernel": k, "launches": c, "total_ms": round(t, 4), "share_pct": round(100 * t / tot, 2)}
            for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])]
     json.dump({"note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised): "
-                       "compare shares, not absolute times", "kernels": res}, open(out, "w"), indent=1)
+                       "compare shares, not absolute times" + (f"; excluded (not part of a step): {exclude}"
+                                                                if exclude else ""),
+               "kernels": res}, open(out, "w"), indent=1)
     for r in res:
         print(f"{r['launches']:5d} {r['total_ms']:9.3f} ms {r['share_pct']:6.2f}%  {r['kernel'][:90]}")
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
-        launches(sys.argv[2], sys.argv[3])
+        launches(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
     else:
         full(sys.argv[1], sys.argv[2])
