@@ -5,8 +5,8 @@ N = 65,536 candidate initial states per GPU, H = 64 networks, gap x std score.
 
 One step (metric 1) = for every candidate: a T-step
 actor rollout with running + terminal cost (K1), critic V(x0) and std sigma(x0)
-(K2), score sigma*|V - J|, a stable top-(N/10) select (K3), and the warm-start
-re-rollout of the kept 1/10 emitting U (K1).  `value` is device-resident
+(K2, fused into the K1 launch), score sigma*|V - J|, a stable top-(N/10) select
+(K3), and the kept 1/10's warm starts U (taken from the K1 controls).  `value` is device-resident
 (inputs already in HBM); `e2e` goes through the public API with the candidate
 states in pinned host memory and the kept indices + warm starts read back.
 
@@ -14,7 +14,11 @@ states in pinned host memory and the kept indices + warm starts read back.
 
 Multi-GPU (torchrun): each rank scores its own 65,536-candidate shard (weak
 scaling), the shard winners are merged exactly with ONE NCCL all-gather, and
-each rank re-rolls its slice of the global kept set.
+each rank returns the warm starts of its slice of the global kept set.
+
+  --workload {dubins, pointmass, manipulator3, aliengo_lipm} selects the other
+  BASELINE.json configs (N per GPU: 65,536 / 750 / 262,144 / 131,072 = the 1M
+AlienGO set sharded 8 ways); the default is configs[1] (dubins).
 """
 
 from __future__ import annotations
@@ -35,6 +39,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "rollout+BIC states scored/sec"
 CONFIG_NAME = "dubins"
 N_PER_GPU = 65536
+WORKLOADS = {"dubins": 65536, "pointmass": 750, "manipulator3": 262144, "aliengo_lipm": 1 << 17}
 HIDDEN = 64
 CAND_MULT = 10
 SEED = 0
@@ -236,12 +241,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cacto", choices=["cacto", "reference"])
-    ap.add_argument("--n", type=int, default=N_PER_GPU, help="candidates per GPU")
+    ap.add_argument("--n", type=int, default=0, help="candidates per GPU (0: the workload's)")
+    ap.add_argument("--workload", default="dubins", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="CPU baseline sample (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
+    global CONFIG_NAME, N_PER_GPU
+    CONFIG_NAME = args.workload
+    N_PER_GPU = WORKLOADS[args.workload]
+    if args.n <= 0:
+        args.n = N_PER_GPU
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -257,7 +268,7 @@ def main():
         if rank != 0:
             return
         cores = len(os.sched_getaffinity(0))
-        sample = args.cpu_sample or max(64, cores * 64)    # ~0.6 s per step
+        sample = min(args.cpu_sample or max(64, cores * 64), N_PER_GPU)    # ~0.6 s per step
         cores, times = run_cpu(spec, field, actor, critic, std, sample, args.steps, max(1, args.warmup))
         sec = float(np.mean(times))
         val = sample / sec
@@ -438,7 +449,7 @@ def main():
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
-        sample = args.cpu_sample or max(128, cores * 128)   # ~10 core-seconds of work
+        sample = min(args.cpu_sample or max(128, cores * 128), N)   # ~10 core-seconds of work
         cores, times = run_cpu(spec, field, actor, critic, std, sample, 1, 1)
         line["cpu_baseline"] = {"value": sample / times[0], "unit": "states/s", "cores": cores, "kind": "port",
                                 "sample": f"{sample} of the {N} candidates through the same pipeline: per-start "
