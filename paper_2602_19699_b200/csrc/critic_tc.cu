@@ -1,0 +1,666 @@
+// critic_tc.cu -- the Sobolev critic loss (nets.critic_loss, nets.py:233-290) on
+// the tensor cores for the 3 x 64 networks of the reference configs, fp32
+// accurate through the 3xFP16 split of tcmlp.cuh.
+//
+// Two stages:
+//  1. critic_tc_kernel -- per 128-sample tile (TMEM lane = sample), every
+//     per-sample matrix product is a tcgen05 layer with A in TMEM: the target
+//     forward at x_{+k} (4 layers), the critic forward at x (4, z_i kept in
+//     TMEM), the input-gradient sweep s_i = g_i W_i (3, transposed weights), the
+//     gradient-path r_i = W_i u_i (3) and the value-path abar_i = zbar_i W_i (2).
+//     The epilogue warps (4 per TMEM lane quadrant, 16 columns each) apply the
+//     activation / its derivatives (nets.py:27-52), form e_v, e_g, the loss and
+//     the cotangents (nets.py:247-289), and stream the per-sample factors of the
+//     weight gradients to HBM: [g_i ; zbar_i] and [u_i ; a_i] as 2B-row matrices.
+//  2. the batch reductions -- gW_i = [g_i ; zbar_i]^T [u_i ; a_i] as one tcgen05
+//     GEMM per layer over K = 2B (gemm_tc.cu, MN-major operands), bias and
+//     output-row gradients as deterministic column sums.  One gradient slot
+//     (n_partials = 1), so the fold / Adam kernels apply unchanged.
+// TMEM (512 columns, one tile per CTA): D [64] | A_hi [32] | A_lo [32] |
+// z_0..z_2 [3 x 64] | g_i -> zeta_i [3 x 64].
+#include "tcmlp.cuh"
+
+namespace cacto {
+
+int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk,
+              float* D, int64_t ldd, int accumulate, float alpha, int passes, void* ws, size_t ws_bytes,
+              cudaStream_t st);
+size_t gemm_workspace_bytes(int M, int N, int K);
+
+namespace ctc {
+
+constexpr int HP = 64;
+constexpr int TILE = 128;
+constexpr int NEPI = 16;  // epilogue warps: 4 per lane quadrant x 16 columns
+constexpr int MMA_WARP = NEPI;
+constexpr int NTHR = NEPI * 32 + 32;
+constexpr uint32_t TD = 0, TA_HI = 64, TA_LO = 96, TZ = 128, TG = 320;
+using PL = rtc::Plan<HP>;
+constexpr uint32_t SLOT = PL::SLOT;             // 0 = critic, 1 = target (forward weights)
+constexpr uint32_t W0T = rtc::NOUT * 128;       // W0^T [16][64] (N = padded input width)
+constexpr uint32_t WHT = HP * 128;              // W_i^T [64][64]
+constexpr uint32_t OFF_W0T = 2 * SLOT;          // hi, lo
+constexpr uint32_t OFF_W1T = OFF_W0T + 2 * W0T;
+constexpr uint32_t OFF_W2T = OFF_W1T + 2 * WHT;
+constexpr uint32_t OFF_W3 = OFF_W2T + 2 * WHT;  // fp32 output row w_3 [64], unscaled
+constexpr uint32_t BYTES = OFF_W3 + HP * 4 + 1024;
+
+struct CBatch {
+  const int64_t* idx;
+  const int64_t* cycle;
+  int64_t idx_stride;
+  const float *xa, *v_bar, *v_bar_x, *xa_plus_k;
+  int64_t rows;
+  int n, t_max;
+  CACTO_D int64_t row(int64_t b) const {
+    if (!idx) return b;
+    return cycle ? idx[(*cycle) * idx_stride + b] : idx[b];
+  }
+};
+
+struct Args {
+  CBatch b;
+  const float* critic;
+  const float* target;  // null: no bootstrap
+  NetConst<float> nc, nc_t;
+  int ip;               // padded input width of W0 (8 or 16)
+  float k_s, inv_denom;
+  // per-sample factors of the weight gradients (rows = b.rows = B)
+  float* GZ[3];  // [2B][64]: g_i rows, then zbar_i rows
+  // [2B][W_i + 4]: u_i rows then a_i rows, plus a bias column (0 on u rows, 1 on
+  // a rows) so one GEMM yields gW_i and gb_i; W_0 = 16, W_1 = W_2 = W_3 = 64
+  float* UA[4];  // UA[3]: u_3 rows then a_3 rows (the output row w_3)
+  float* V3;     // [2B]: 1 on u_3 rows, -2 e_v on a_3 rows (left factor of gW_3, gb_3)
+  float* lossp;  // [gridDim.x]
+};
+
+// transposed copy: element (r = c, k = o) = W[o][c] * scale, K-major SW128 fp16
+CACTO_D void stage_wt(unsigned char* hi, unsigned char* lo, const float* W, int out, int in, int stride, float scale,
+                      int rrows, int tid, int nthr) {
+  for (int e = tid; e < rrows * HP; e += nthr) {
+    const int c = e / HP, o = e - c * HP;
+    const float v = (c < in && o < out) ? W[(int64_t)o * stride + c] * scale : 0.f;
+    const __half h = __float2half_rn(v);
+    const uint32_t off = rtc::sw128h(c, o);
+    *reinterpret_cast<__half*>(hi + off) = h;
+    *reinterpret_cast<__half*>(lo + off) = __float2half_rn(v - __half2float(h));
+  }
+}
+
+// one product layer: KSTEPS k-steps of 3 MMAs; `zero` starts a fresh accumulator
+template <int KSTEPS>
+CACTO_D void issue(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc, bool zero) {
+#pragma unroll
+  for (int kk = 0; kk < KSTEPS; ++kk) {
+    const uint64_t wo = (uint64_t)(kk * 2);
+    const uint32_t ao = (uint32_t)(kk * 8);
+    tc::mma_f16_ts_elect(d, ahi + ao, whi + wo, idesc, (zero && kk == 0) ? 0u : 1u);
+    tc::mma_f16_ts_elect(d, ahi + ao, wlo + wo, idesc, 1u);
+    tc::mma_f16_ts_elect(d, alo + ao, whi + wo, idesc, 1u);
+  }
+}
+
+// derivative factors of the activation at z (nets.py:27-52): d1 = act'(z),
+// h with act''(z) = h * act'(z)
+template <int ACT>
+CACTO_D void d1h(float z, float& d1, float& h) {
+  if constexpr (ACT == CACTO_ACT_ELU) {
+    const float e = tc::ex2_ftz(fminf(z, 0.f) * rtc::LOG2E);
+    d1 = z > 0.f ? 1.f : e;
+    h = z > 0.f ? 0.f : 1.f;
+  } else {
+    const float t = tanhf(z);
+    d1 = 1.f - t * t;
+    h = -2.f * t;
+  }
+}
+
+CACTO_D void st16g(float* dst, const float (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+}
+
+}  // namespace ctc
+
+template <int ACT>
+__global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args a) {
+  using namespace ctc;
+  using AF = ActTC<ACT>;
+  constexpr float S = AF::S;            // forward / transposed hidden-layer weight scale
+  constexpr float SO = rtc::WSCALE;     // output-layer weight scale
+  // backward operands (g, u, zbar) enter the MMAs scaled by SB and the cotangents
+  // are carried without the 1/B of the mean (applied in the reductions): both keep
+  // the fp16 lo parts out of the subnormal range
+  constexpr float SB = 16.f;
+  constexpr float RS = 1.f / (S * SB);  // backward product -> value
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar, done_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float red[NTHR / 32];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ip = a.ip;
+  const int n = a.b.n;
+  const int d = n + 1;
+
+  // ---- weights -> shared memory ----------------------------------------------------
+  if (ip == 8) {
+    stage_net<HP, 8, AF>(base, a.critic, 3, d, 1, threadIdx.x, NTHR);
+    if (a.target) stage_net<HP, 8, AF>(base + SLOT, a.target, 3, d, 1, threadIdx.x, NTHR);
+  } else {
+    stage_net<HP, 16, AF>(base, a.critic, 3, d, 1, threadIdx.x, NTHR);
+    if (a.target) stage_net<HP, 16, AF>(base + SLOT, a.target, 3, d, 1, threadIdx.x, NTHR);
+  }
+  {
+    const float* W0 = a.critic;
+    const float* W1 = W0 + HP * ip + HP;
+    const float* W2 = W1 + HP * HP + HP;
+    const float* W3 = W2 + HP * HP + HP;
+    stage_wt(base + OFF_W0T, base + OFF_W0T + W0T, W0, HP, d, ip, S, rtc::NOUT, threadIdx.x, NTHR);
+    stage_wt(base + OFF_W1T, base + OFF_W1T + WHT, W1, HP, HP, HP, S, HP, threadIdx.x, NTHR);
+    stage_wt(base + OFF_W2T, base + OFF_W2T + WHT, W2, HP, HP, HP, S, HP, threadIdx.x, NTHR);
+    float* w3 = reinterpret_cast<float*>(base + OFF_W3);
+    for (int c = threadIdx.x; c < HP; c += NTHR) w3[c] = W3[c];
+  }
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&full_bar, NEPI);
+    tc::mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) tc::tmem_alloc(&tmem_base_sh, 512);
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t sbase = saddr(base);
+  const int64_t B = a.b.rows;
+  const int64_t ntiles = (B + TILE - 1) / TILE;
+  const bool boot = a.target != nullptr;
+  const int nops = (boot ? 4 : 0) + 4 + 3 + 3 + 2;
+
+  if (warp < NEPI) {
+    // ---- epilogue ------------------------------------------------------------------
+    const int q = warp & 3, part = warp >> 2;
+    const int r = (q << 5) + lane;
+    const int c0 = part * 16;  // my accumulator columns [c0, c0 + 16)
+    const uint32_t lrow = tmem + ((uint32_t)(q * 32) << 16);
+    const bool owner = part == 0;
+    const float* w3 = reinterpret_cast<const float*>(base + OFF_W3);
+    const uint32_t bias_c = sbase + PL::off_bias, bias_t = sbase + SLOT + PL::off_bias;
+    uint32_t pd = 0;
+    float loss_acc = 0.f;
+    auto handoff = [&]() {
+      tc::tmem_wait_st();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full_bar);
+    };
+    auto wait_done = [&]() {
+      tc::mbar_wait_sleep(&done_bar, pd);
+      pd ^= 1;
+      tc::tc_fence_after();
+    };
+    auto ld16 = [&](uint32_t col, float (&v)[16]) { tc::tmem_ld16_wait(lrow + col, v); };
+    auto st16 = [&](uint32_t col, const float (&v)[16]) { tc::tmem_st16(lrow + col, v); };
+    // my 16 values -> next layer's A (hi/lo), columns [c0, c0 + 16) of the operand
+    auto put_a = [&](const float (&v)[16]) {
+      float hv[8], lv[8];
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) {
+        uint32_t h, l;
+        rtc::split2(v[c], v[c + 1], h, l);
+        hv[c / 2] = __uint_as_float(h);
+        lv[c / 2] = __uint_as_float(l);
+      }
+      tc::tmem_st8(lrow + TA_HI + (uint32_t)(c0 / 2), hv);
+      tc::tmem_st8(lrow + TA_LO + (uint32_t)(c0 / 2), lv);
+    };
+    auto put_ab = [&](const float (&v)[16]) {  // backward operand, scaled by SB
+      float w[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) w[c] = v[c] * SB;
+      put_a(w);
+    };
+    auto preload_bias = [&](uint32_t col, uint32_t bias_s, int layer) {
+      float bv[16];
+#pragma unroll
+      for (int c = 0; c < 16; c += 4) {
+        const V4<float> v = lds4(bias_s + (uint32_t)((layer * HP + c0 + c) * 4), (float*)nullptr);
+        bv[c] = v.v[0]; bv[c + 1] = v.v[1]; bv[c + 2] = v.v[2]; bv[c + 3] = v.v[3];
+      }
+      st16(col + (uint32_t)c0, bv);  // my columns of the layer's accumulator
+    };
+    auto preload_out_bias = [&](uint32_t bias_s) {  // output layer: D columns 0..15 (part 0)
+      if (!owner) return;
+      float bv[16];
+#pragma unroll
+      for (int c = 0; c < 16; c += 4) {
+        const V4<float> v = lds4(bias_s + (uint32_t)((3 * HP + c) * 4), (float*)nullptr);
+        bv[c] = v.v[0]; bv[c + 1] = v.v[1]; bv[c + 2] = v.v[2]; bv[c + 3] = v.v[3];
+      }
+      st16(TD, bv);
+    };
+    // the owner's normalised input row (16 columns) -> A
+    auto put_input = [&](const float (&v)[16]) {
+      if (!owner) return;
+      put_a(v);
+    };
+
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t gb = t * TILE + r;
+      const bool valid = gb < B;
+      const int64_t rr = valid ? a.b.row(gb) : 0;
+      float y = 0.f;
+      float xin[16];
+      // ---- target forward at x_{+k} (nets.py:247-251) --------------------------------
+      if (boot) {
+        if (owner) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) xin[c] = 0.f;
+          if (valid) {
+            const float* xk = a.b.xa_plus_k + rr * d;
+            for (int c = 0; c < d; ++c) xin[c] = (xk[c] - a.nc_t.in_center[c]) / a.nc_t.in_half[c];
+          }
+        }
+        put_input(xin);
+        preload_bias(TD, bias_t, 0);
+        handoff();
+        for (int l = 0; l < 3; ++l) {
+          wait_done();
+          float z[16];
+          ld16(TD + c0, z);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) z[c] = AF::apply(z[c]);
+          put_a(z);
+          if (l < 2) preload_bias(TD, bias_t, l + 1);
+          else preload_out_bias(bias_t);
+          handoff();
+        }
+        wait_done();
+        if (owner) {
+          float o[16];
+          ld16(TD, o);
+          if (valid) {
+            const float vt = o[0] * (1.f / SO);
+            const bool gate = a.b.xa_plus_k[rr * d + n] < (float)a.b.t_max;
+            y = gate ? vt : 0.f;
+          }
+        }
+      }
+      // ---- critic forward at x, z_i kept in TMEM -------------------------------------
+      if (owner) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) xin[c] = 0.f;
+        if (valid) {
+          const float* x = a.b.xa + rr * d;
+          for (int c = 0; c < d; ++c) xin[c] = (x[c] - a.nc.in_center[c]) / a.nc.in_half[c];
+          y += a.b.v_bar[rr];
+          st16g(a.UA[0] + (B + gb) * 20, xin);  // a_0 = normalised input
+          *reinterpret_cast<float4*>(a.UA[0] + (B + gb) * 20 + 16) = make_float4(1.f, 0.f, 0.f, 0.f);
+        }
+      }
+      put_input(xin);
+      preload_bias(TZ, bias_c, 0);
+      handoff();
+      for (int l = 0; l < 3; ++l) {
+        wait_done();
+        float z[16];
+        ld16(TZ + 64 * l + c0, z);
+        float av[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) av[c] = AF::apply(z[c]);
+        put_a(av);
+        if (valid) {
+          float* row = a.UA[l + 1] + (B + gb) * 68;
+          st16g(row + c0, av);
+          if (owner) *reinterpret_cast<float4*>(row + 64) = make_float4(1.f, 0.f, 0.f, 0.f);
+        }
+        if (l < 2) preload_bias(TZ + 64 * (l + 1), bias_c, l + 1);
+        else preload_out_bias(bias_c);
+        handoff();
+      }
+      // output: V, e_v, delta; then the sweep starts: g_2 = act'(z_2) w_3
+      wait_done();
+      float ev = 0.f, delta = 0.f;
+      if (owner) {
+        float o[16];
+        ld16(TD, o);
+        if (valid) {
+          ev = y - o[0] * (1.f / SO);
+          delta = -2.f * ev;  // x 1/denom in the reductions
+          a.V3[gb] = 1.f;
+          a.V3[B + gb] = delta;
+        }
+      }
+      {
+        float z[16], g[16];
+        ld16(TZ + 128 + c0, z);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float d1, h;
+          d1h<ACT>(z[c] * (1.f / S), d1, h);
+          g[c] = d1 * w3[c0 + c];
+        }
+        st16(TG + 128 + c0, g);
+        if (valid) st16g(a.GZ[2] + gb * 64 + c0, g);
+        put_ab(g);
+        handoff();  // S2: s_2 = g_2 W_2
+      }
+      for (int l = 1; l >= 0; --l) {  // g_l = act'(z_l) s_{l+1}
+        wait_done();
+        float s[16], z[16], g[16];
+        tc::tmem_ld16x2_wait(lrow + TD + c0, lrow + TZ + 64 * l + c0, s, z);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float d1, h;
+          d1h<ACT>(z[c] * (1.f / S), d1, h);
+          g[c] = d1 * s[c] * RS;
+        }
+        st16(TG + 64 * l + c0, g);
+        if (valid) st16g(a.GZ[l] + gb * 64 + c0, g);
+        put_ab(g);
+        handoff();  // S1: s_1 = g_1 W_1 ; S0: s_0 = g_0 W_0 (N = 16)
+      }
+      // errors, loss, u_0 (nets.py:268-277)
+      wait_done();
+      {
+        float u0[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) u0[c] = 0.f;
+        if (owner) {
+          float s0[16];
+          ld16(TD, s0);
+          if (valid) {
+            const float* vx = a.b.v_bar_x + rr * n;
+            float eg2 = 0.f;
+            const float coef = -2.f * a.k_s;  // x 1/denom in the reductions
+            for (int c = 0; c < n; ++c) {
+              const float eg = vx[c] - s0[c] * RS / a.nc.in_half[c];
+              eg2 += eg * eg;
+              u0[c] = coef * eg / a.nc.in_half[c];
+            }
+            loss_acc += (ev * ev + a.k_s * eg2) * a.inv_denom;
+            st16g(a.UA[0] + gb * 20, u0);
+            *reinterpret_cast<float4*>(a.UA[0] + gb * 20 + 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        if (owner) put_ab(u0);
+        handoff();  // R0: r_0 = W_0 u_0
+      }
+      // gradient path (nets.py:279-284): zeta_l = h(z_l) g_l r_l, u_{l+1} = act'(z_l) r_l
+      for (int l = 0; l < 3; ++l) {
+        wait_done();
+        float rv[16], z[16], g[16], u[16];
+        tc::tmem_ld16x3_wait(lrow + TD + c0, lrow + TZ + 64 * l + c0, lrow + TG + 64 * l + c0, rv, z, g);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float d1, h;
+          d1h<ACT>(z[c] * (1.f / S), d1, h);
+          const float rr_ = rv[c] * RS;
+          g[c] = h * g[c] * rr_;  // zeta_l
+          u[c] = d1 * rr_;
+        }
+        st16(TG + 64 * l + c0, g);
+        if (l < 2) {
+          if (valid) {
+            float* row = a.UA[l + 1] + gb * 68;
+            st16g(row + c0, u);
+            if (owner) *reinterpret_cast<float4*>(row + 64) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          put_ab(u);
+          handoff();  // R1, R2
+        } else {
+          if (valid) {
+            float* row = a.UA[3] + gb * 68;
+            st16g(row + c0, u);
+            if (owner) *reinterpret_cast<float4*>(row + 64) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      }
+      float zb[16];
+      // value path (nets.py:287-289, 215-230): abar_3 = delta w_3,
+      // zbar_2 = act'(z_2) abar_3 + zeta_2; delta lives in the quadrant's owner thread
+      {
+        __shared__ float del_sh[TILE];
+        if (owner) del_sh[r] = delta;
+        // epilogue warps only: a named barrier over the 16 epilogue warps
+        asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory");
+        const float dlt = del_sh[r];
+        float z[16], zeta[16];
+        tc::tmem_ld16x2_wait(lrow + TZ + 128 + c0, lrow + TG + 128 + c0, z, zeta);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float d1, h;
+          d1h<ACT>(z[c] * (1.f / S), d1, h);
+          zb[c] = d1 * (dlt * w3[c0 + c]) + zeta[c];
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory");  // del_sh reused next tile
+      }
+      if (valid) st16g(a.GZ[2] + (B + gb) * 64 + c0, zb);
+      put_ab(zb);
+      handoff();  // B2: abar_2 = zbar_2 W_2
+      for (int l = 1; l >= 0; --l) {
+        wait_done();
+        float ab[16], z[16], zeta[16];
+        tc::tmem_ld16x3_wait(lrow + TD + c0, lrow + TZ + 64 * l + c0, lrow + TG + 64 * l + c0, ab, z, zeta);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float d1, h;
+          d1h<ACT>(z[c] * (1.f / S), d1, h);
+          zb[c] = d1 * ab[c] * RS + zeta[c];
+        }
+        if (valid) st16g(a.GZ[l] + (B + gb) * 64 + c0, zb);
+        if (l == 1) {
+          put_ab(zb);
+          handoff();  // B1: abar_1 = zbar_1 W_1
+        }
+      }
+    }
+    // loss partial of this CTA
+    float v = loss_acc;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory");
+    if (threadIdx.x == 0) {
+      float s = 0.f;
+      for (int w = 0; w < NEPI; ++w) s += red[w];
+      a.lossp[blockIdx.x] = s;
+    }
+  } else {
+    // ---- MMA issuer --------------------------------------------------------------------
+    const uint32_t i64 = tc::idesc_f16(HP), i16 = tc::idesc_f16(rtc::NOUT);
+    auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
+    const uint32_t ahi = tmem + TA_HI, alo = tmem + TA_LO;
+    uint32_t pf = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int op = 0; op < nops; ++op) {
+        tc::mbar_wait_sleep(&full_bar, pf);
+        pf ^= 1;
+        tc::tc_fence_after();
+        const int k = boot ? op : op + 4;  // op index in the full list (targets first)
+        if (k < 8) {  // forward layers: target (k < 4) or critic (4 <= k < 8)
+          const uint32_t so = k < 4 ? SLOT : 0u;
+          const int l = k & 3;
+          const uint32_t dcol = (k >= 4 && l < 3) ? tmem + TZ + 64 * l : tmem + TD;
+          if (l == 0) issue<1>(dcol, ahi, alo, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), i64, false);
+          else if (l < 3)
+            issue<4>(dcol, ahi, alo, desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH),
+                     desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH + PL::WH), i64, false);
+          else issue<4>(dcol, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), i16, false);
+        } else if (k == 8) {
+          issue<4>(tmem + TD, ahi, alo, desc(OFF_W2T), desc(OFF_W2T + WHT), i64, true);  // s_2
+        } else if (k == 9) {
+          issue<4>(tmem + TD, ahi, alo, desc(OFF_W1T), desc(OFF_W1T + WHT), i64, true);  // s_1
+        } else if (k == 10) {
+          issue<4>(tmem + TD, ahi, alo, desc(OFF_W0T), desc(OFF_W0T + W0T), i16, true);  // s_0
+        } else if (k == 11) {
+          issue<1>(tmem + TD, ahi, alo, desc(PL::off_w0), desc(PL::off_w0 + PL::W0), i64, true);  // r_0
+        } else if (k == 12 || k == 13) {
+          const uint32_t wo = PL::off_wh + (uint32_t)(2 * (k - 12)) * PL::WH;
+          issue<4>(tmem + TD, ahi, alo, desc(wo), desc(wo + PL::WH), i64, true);  // r_1, r_2
+        } else if (k == 14) {
+          issue<4>(tmem + TD, ahi, alo, desc(OFF_W2T), desc(OFF_W2T + WHT), i64, true);  // abar_2
+        } else {
+          issue<4>(tmem + TD, ahi, alo, desc(OFF_W1T), desc(OFF_W1T + WHT), i64, true);  // abar_1
+        }
+        tc::tc_commit_elect(&done_bar);
+        __syncwarp();
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) tc::tmem_dealloc(tmem, 512);
+}
+
+// ======================================================================================
+// host side
+// ======================================================================================
+namespace ctc {
+
+struct Plan2 {  // workspace carve
+  size_t off_gz[3], off_ua[4], off_v3, off_t[4], off_lossp, off_gemm, total;
+};
+
+static Plan2 plan2(int64_t B, int64_t P) {
+  Plan2 p{};
+  size_t o = ((size_t)(P + 1) * 4 + 255) & ~(size_t)255;  // gradient slot first
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 255) & ~(size_t)255;
+    return r;
+  };
+  for (int l = 0; l < 3; ++l) p.off_gz[l] = take((size_t)2 * B * HP * 4);
+  p.off_ua[0] = take((size_t)2 * B * 20 * 4);
+  for (int l = 1; l < 4; ++l) p.off_ua[l] = take((size_t)2 * B * 68 * 4);
+  p.off_v3 = take((size_t)2 * B * 4 + 16);
+  for (int l = 0; l < 4; ++l) p.off_t[l] = take((size_t)HP * 68 * 4);
+  p.off_lossp = take((size_t)4096 * 4);
+  size_t g = gemm_workspace_bytes(HP, 65, (int)(2 * B));
+  size_t g2 = gemm_workspace_bytes(1, 65, (int)(2 * B));
+  p.off_gemm = take(g > g2 ? g : g2);
+  p.total = o + 256;
+  return p;
+}
+
+// T_l [64][17 or 65] -> gW_l (first cols) and gb_l (bias column); T_3 [1][65] -> w_3, b_3
+__global__ void scatter_grads_kernel(const float* __restrict__ T0, const float* __restrict__ T1,
+                                     const float* __restrict__ T2, const float* __restrict__ T3, int cols0,
+                                     float* slot, int64_t w0, int64_t b0, int64_t w1, int64_t b1, int64_t w2,
+                                     int64_t b2, int64_t w3, int64_t b3) {
+  const int l = blockIdx.x;
+  if (l < 3) {
+    const float* T = l == 0 ? T0 : (l == 1 ? T1 : T2);
+    const int cols = l == 0 ? cols0 : HP, N = l == 0 ? 17 : 65, bc = l == 0 ? 16 : 64;
+    float* gw = slot + (l == 0 ? w0 : (l == 1 ? w1 : w2));
+    float* gbv = slot + (l == 0 ? b0 : (l == 1 ? b1 : b2));
+    for (int e = threadIdx.x; e < HP * cols; e += blockDim.x) gw[e] += T[(e / cols) * N + (e % cols)];
+    for (int m = threadIdx.x; m < HP; m += blockDim.x) gbv[m] += T[m * N + bc];
+  } else {
+    for (int c = threadIdx.x; c < HP; c += blockDim.x) slot[w3 + c] += T3[c];
+    if (threadIdx.x == 0) slot[b3] += T3[64];
+  }
+}
+__global__ void loss_fold_kernel(const float* __restrict__ part, int n, float* dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    float s = 0.f;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *dst = s;
+  }
+}
+
+}  // namespace ctc
+
+bool critic_tc_enabled() {
+  const char* e = getenv("CACTO_CRITIC_TC");  // 0: fused SIMT kernel (A/B measurements)
+  return !e || atoi(e) != 0;
+}
+
+// eligible: fp32, 3 hidden layers of padded width 64, input n + 1 <= 16, target
+// (if any) of the same shape; the batch large enough to fill the GPU with tiles
+bool critic_tc_eligible(const cacto_mlp_t* c, const cacto_mlp_t* tgt, int64_t rows) {
+  if (!critic_tc_enabled() || !c || c->dtype != CACTO_F32 || c->n_layers != 4 || c->hp != 64 || c->sizes[0] > 16 ||
+      c->sizes[4] != 1)
+    return false;
+  if (tgt && (tgt->dtype != CACTO_F32 || tgt->n_layers != 4 || tgt->hp != 64 || tgt->sizes[0] != c->sizes[0] ||
+              tgt->activation != c->activation))
+    return false;
+  const char* e = getenv("CACTO_CRITIC_TC_MIN");  // minimum batch (default: 32 tiles per SM-wave)
+  const int64_t min_rows = e ? atoll(e) : (int64_t)8192;
+  return rows >= min_rows;
+}
+
+size_t critic_tc_workspace_bytes(const cacto_mlp_t* c, int64_t rows) {
+  NetShape sh = shape_of(*c);
+  return ctc::plan2(rows > 0 ? rows : 1, layer_offsets(sh).total).total;
+}
+
+int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_batch_t* bt, double k_s, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  using namespace ctc;
+  NetShape sh = shape_of(*c);
+  LayerOffsets lo = layer_offsets(sh);
+  const int64_t B = bt->rows;
+  Plan2 p = plan2(B, lo.total);
+  if (ws_bytes < p.total) return set_error(CACTO_EVALUE, "critic_loss(tc): workspace too small");
+  char* w = (char*)ws;
+  float* slot = (float*)w;
+  cudaMemsetAsync(slot, 0, (size_t)(lo.total + 1) * 4, st);
+  Args a{};
+  a.b.idx = bt->idx;
+  a.b.cycle = bt->cycle;
+  a.b.idx_stride = bt->idx_stride;
+  a.b.xa = (const float*)bt->xa;
+  a.b.v_bar = (const float*)bt->v_bar;
+  a.b.v_bar_x = (const float*)bt->v_bar_x;
+  a.b.xa_plus_k = (const float*)bt->xa_plus_k;
+  a.b.rows = B;
+  a.b.n = bt->n;
+  a.b.t_max = bt->t_max;
+  a.critic = (const float*)c->params;
+  a.target = tgt ? (const float*)tgt->params : nullptr;
+  a.nc = net_const<float>(*c);
+  a.nc_t = tgt ? net_const<float>(*tgt) : a.nc;
+  a.ip = sh.ip;
+  a.k_s = (float)k_s;
+  a.inv_denom = 1.f / (float)(bt->denom > 0 ? bt->denom : B);
+  for (int l = 0; l < 3; ++l) a.GZ[l] = (float*)(w + p.off_gz[l]);
+  for (int l = 0; l < 4; ++l) a.UA[l] = (float*)(w + p.off_ua[l]);
+  a.V3 = (float*)(w + p.off_v3);
+  a.lossp = (float*)(w + p.off_lossp);
+  const int64_t ntiles = (B + TILE - 1) / TILE;
+  const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+  auto kern = c->activation == CACTO_ACT_ELU ? critic_tc_kernel<CACTO_ACT_ELU> : critic_tc_kernel<CACTO_ACT_TANH>;
+  if (!ensure_smem((const void*)kern, BYTES))
+    return set_error(CACTO_ECUDA, "critic_loss(tc): %u B of shared memory not available", BYTES);
+  kern<<<grid, NTHR, BYTES, st>>>(a);
+  int rc = check_launch("critic_tc_kernel");
+  if (rc) return rc;
+  // batch reductions: per layer ONE GEMM over K = 2B gives the weight gradient and,
+  // from the bias column, the bias gradient; the output row w_3 and b_3 from a
+  // 1-row GEMM with the [1 ; -2 e_v] factor.  Results (scaled by 1/denom) land in
+  // small [rows][N] tiles that one kernel adds into the padded gradient slot.
+  void* gws = w + p.off_gemm;
+  const size_t gwb = p.total - p.off_gemm - 256;
+  const int ncol[4] = {17, 65, 65, 65};
+  const int wpad[4] = {20, 68, 68, 68};
+  float* T[4];
+  for (int l = 0; l < 4; ++l) T[l] = (float*)(w + p.off_t[l]);
+  for (int l = 0; l < 3; ++l) {
+    rc = gemm_tf32(HP, ncol[l], (int)(2 * B), a.GZ[l], 1, HP, a.UA[l], 1, wpad[l], T[l], ncol[l], 0, a.inv_denom, 3,
+                   gws, gwb, st);
+    if (rc) return rc;
+  }
+  const int64_t K2 = 2 * B;
+  rc = gemm_tf32(1, 65, (int)K2, a.V3, (K2 + 3) / 4 * 4, 1, a.UA[3], 1, 68, T[3], 65, 0, a.inv_denom, 3, gws, gwb,
+                 st);
+  if (rc) return rc;
+  scatter_grads_kernel<<<4, 256, 0, st>>>(T[0], T[1], T[2], T[3], lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1],
+                                          lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);
+  loss_fold_kernel<<<1, 32, 0, st>>>(a.lossp, grid, slot + lo.total);
+  return check_launch("critic_tc reductions");
+}
+
+}  // namespace cacto

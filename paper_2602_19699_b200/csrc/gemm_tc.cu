@@ -300,6 +300,26 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
   }
 }
 
+// many splits (small output, long K): one warp per output element, lanes over
+// the splits, a fixed shuffle tree -- deterministic
+__global__ void splitk_reduce_warp_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int M,
+                                          int N, float* D, int64_t ldd, int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total;
+       e += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float s = 0.f;
+    for (int z = lane; z < splits; z += 32) s += part[z * split_stride + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int64_t m = e / N, n = e - m * N;
+      float* d = D + m * ldd + n;
+      *d = accumulate ? *d + s : s;
+    }
+  }
+}
+
 }  // namespace tc
 
 // workspace bytes a gemm of this shape may need for split-K partials
@@ -349,6 +369,13 @@ int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, con
   if (rc || splits == 1) return rc;
   int64_t total = (int64_t)M * N;
   unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 8 * num_sms());
+  if (splits >= 16) {
+    const int64_t warps = total;
+    unsigned g2 = (unsigned)std::min<int64_t>((warps * 32 + 255) / 256, 16 * num_sms());
+    tc::splitk_reduce_warp_kernel<<<g2, 256, 0, st>>>((const float*)ws, splits, (int64_t)M * N, M, N, D, ldd,
+                                                      accumulate);
+    return check_launch("splitk_reduce_warp_kernel");
+  }
   tc::splitk_reduce_kernel<<<grid, 256, 0, st>>>((const float*)ws, splits, (int64_t)M * N, M, N, N, D, ldd, accumulate);
   return check_launch("splitk_reduce_kernel");
 }

@@ -32,139 +32,9 @@
 #include "rollout.cuh"
 #include "systems.cuh"
 #include "tc.cuh"
+#include "tcmlp.cuh"
 
 namespace cacto {
-
-namespace rtc {
-
-constexpr int TILE = 128;
-constexpr int NOUT = 16;        // output-layer MMA width (m <= 8 used)
-constexpr int KIN = 16;         // input-layer K (n + 1 <= 16, zero padded)
-constexpr float WSCALE = 8.f;   // 2^3 weight pre-scale
-constexpr float LOG2E = 1.4426950408889634f;
-
-// shared-memory plan (bytes, from a 1024-aligned base); fp16 K-major SW128
-// operands: rows of 128 B = 64 halves
-template <int HP>
-struct Plan {
-  static constexpr uint32_t W0 = HP * 128;    // [HP][16 used]
-  static constexpr uint32_t WH = HP * 128;    // [HP][HP]   (HP <= 64)
-  static constexpr uint32_t WO = NOUT * 128;  // [16][HP]
-  static constexpr uint32_t off_w0 = 0;       // hi, lo
-  static constexpr uint32_t off_wh = off_w0 + 2 * W0;  // (hi, lo) x (nh - 1), nh <= 3
-  static constexpr uint32_t off_wo = off_wh + 2 * 2 * WH;
-  static constexpr uint32_t off_bias = off_wo + 2 * WO;  // fp32 [3][HP] + [NOUT], scaled
-  // one network's slot (1024-aligned); slot 0 = actor, 1..2 = the scoring nets
-  static constexpr uint32_t SLOT = (off_bias + (3 * HP + NOUT) * 4 + 1023) / 1024 * 1024;
-};
-template <int HP, int NT>
-struct Tmem {
-  static constexpr uint32_t PER_TILE = 2 * HP;  // D | A_hi | A_lo
-  static constexpr uint32_t COLS = NT * PER_TILE <= 128 ? 128 : (NT * PER_TILE <= 256 ? 256 : 512);
-  static_assert(NT * PER_TILE <= 512, "TMEM: 2*HP columns per tile");
-};
-
-// byte offset of fp16 element (r, k) in a K-major SW128 operand (k < 64)
-CACTO_HD uint32_t sw128h(int r, int k) {
-  return (uint32_t)(r * 128 + ((((k * 2) >> 4) ^ (r & 7)) << 4) + ((k * 2) & 15));
-}
-
-CACTO_D uint32_t pack_h2(float lo_k, float hi_k) {  // low half = even k
-  __half2 h = __floats2half2_rn(lo_k, hi_k);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-// x = hi + lo, both fp16, for a pair of consecutive k
-CACTO_D void split2(float v0, float v1, uint32_t& hi, uint32_t& lo) {
-  __half2 h = __floats2half2_rn(v0, v1);
-  const float2 hf = __half22float2(h);
-  hi = *reinterpret_cast<uint32_t*>(&h);
-  lo = pack_h2(v0 - hf.x, v1 - hf.y);
-}
-
-// stage W (row-major [rows][cols], stride) * scale as hi/lo fp16 K-major SW128
-// operands of rrows x kcols (zero padded); kcols <= 64
-CACTO_D void stage_w(unsigned char* hi, unsigned char* lo, const float* src, int rows, int cols, int stride,
-                     float scale, int rrows, int kcols, int tid, int nthr) {
-  for (int e = tid; e < rrows * kcols; e += nthr) {
-    const int r = e / kcols, c = e - r * kcols;
-    const float v = (r < rows && c < cols) ? src[(int64_t)r * stride + c] * scale : 0.f;
-    const __half h = __float2half_rn(v);
-    const uint32_t o = sw128h(r, c);
-    *reinterpret_cast<__half*>(hi + o) = h;
-    *reinterpret_cast<__half*>(lo + o) = __float2half_rn(v - __half2float(h));
-  }
-}
-
-// scaled bias of one layer: scale * (b - shift * rowsum(W)) over the real columns
-CACTO_D void stage_bias(float* dst, const float* W, const float* b, int rows, int cols, int stride, float scale,
-                        bool shift, int rrows, int tid, int nthr) {
-  for (int r = tid; r < rrows; r += nthr) {
-    float v = 0.f;
-    if (r < rows) {
-      float s = 0.f;
-      if (shift)
-        for (int c = 0; c < cols; ++c) s += W[(int64_t)r * stride + c];
-      v = scale * (b[r] - s);
-    }
-    dst[r] = v;
-  }
-}
-
-// one layer of one tile: KSTEPS k-steps of hi*hi + hi*lo + lo*hi (A from TMEM);
-// D was pre-loaded with the bias, so every MMA accumulates
-template <int KSTEPS>
-CACTO_D void issue_layer(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc) {
-#pragma unroll
-  for (int kk = 0; kk < KSTEPS; ++kk) {
-    const uint64_t wo = (uint64_t)(kk * 2);  // 32 bytes = 16 halves, in 16-byte units
-    const uint32_t ao = (uint32_t)(kk * 8);  // 16 halves = 8 TMEM columns
-    tc::mma_f16_ts_elect(d, ahi + ao, whi + wo, idesc, 1u);
-    tc::mma_f16_ts_elect(d, ahi + ao, wlo + wo, idesc, 1u);
-    tc::mma_f16_ts_elect(d, alo + ao, whi + wo, idesc, 1u);
-  }
-}
-
-}  // namespace rtc
-
-template <int ACT>
-struct ActTC {
-  // hidden/input layers: D = S * z (ELU: S = 8 log2 e, tanh: S = 8)
-  static constexpr float S = ACT == CACTO_ACT_ELU ? rtc::WSCALE * rtc::LOG2E : rtc::WSCALE;
-  // (feeding ELU(z) + 1 forward and folding the -1 into the next bias saves one
-  // FADD per element but adds ~2^-22 absolute error to every activation near 0:
-  // 5x the output error in an fp64 emulation, so the shift is not used)
-  static constexpr bool SHIFT = false;
-  CACTO_D static float apply(float d) {
-    if constexpr (ACT == CACTO_ACT_ELU) {
-      const float e = tc::ex2_ftz(fminf(d, 0.f) * (1.f / rtc::WSCALE)) - 1.f;
-      return fmaf(fmaxf(d, 0.f), 1.f / S, e);
-    } else {
-      return tanhf(d * (1.f / S));
-    }
-  }
-};
-
-// stage one network into its shared-memory slot: scaled hi/lo fp16 weights and
-// scaled biases (padded layout of include/cacto_b200.h)
-template <int HP, int IP, typename AF>
-CACTO_D void stage_net(unsigned char* slot, const float* P, int nh, int in, int out, int tid, int nthr) {
-  using PL = rtc::Plan<HP>;
-  const int64_t b0 = (int64_t)HP * IP;
-  float* bias = reinterpret_cast<float*>(slot + PL::off_bias);
-  rtc::stage_w(slot + PL::off_w0, slot + PL::off_w0 + PL::W0, P, HP, in, IP, AF::S, HP, rtc::KIN, tid, nthr);
-  rtc::stage_bias(bias, P, P + b0, HP, in, IP, AF::S, false, HP, tid, nthr);
-  int64_t off = b0 + HP;
-  for (int i = 1; i < nh; ++i) {
-    unsigned char* hi = slot + PL::off_wh + (uint32_t)(2 * (i - 1)) * PL::WH;
-    rtc::stage_w(hi, hi + PL::WH, P + off, HP, HP, HP, AF::S, HP, HP, tid, nthr);
-    rtc::stage_bias(bias + i * HP, P + off, P + off + (int64_t)HP * HP, HP, HP, HP, AF::S, AF::SHIFT, HP, tid, nthr);
-    off += (int64_t)HP * HP + HP;
-  }
-  rtc::stage_w(slot + PL::off_wo, slot + PL::off_wo + PL::WO, P + off, out, HP, HP, rtc::WSCALE, rtc::NOUT, HP, tid,
-               nthr);
-  rtc::stage_bias(bias + 3 * HP, P + off, P + off + (int64_t)out * HP, out, HP, HP, rtc::WSCALE, AF::SHIFT, rtc::NOUT,
-                  tid, nthr);
-}
 
 template <int SYS, int HP, int NT, int SPLIT, int ACT>
 __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(const RolloutArgs<float> a) {

@@ -588,6 +588,11 @@ int wide_std_loss(const cacto_mlp_t* sm, const cacto_mlp_t* cm, const cacto_batc
                   cudaStream_t st);
 int wide_actor_loss(const cacto_mlp_t* am, const cacto_mlp_t* cm, const cacto_system_t* sys, const cacto_cost_t* cost,
                     const cacto_batch_t* bt, const int64_t* live, void* ws, size_t ws_bytes, cudaStream_t st);
+// critic_tc.cu (3 x 64 critic on the tensor cores, large batches)
+bool critic_tc_eligible(const cacto_mlp_t* c, const cacto_mlp_t* tgt, int64_t rows);
+size_t critic_tc_workspace_bytes(const cacto_mlp_t* c, int64_t rows);
+int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_batch_t* bt, double k_s, void* ws,
+                   size_t ws_bytes, cudaStream_t st);
 }  // namespace cacto
 int cacto_forward_rows(const cacto_mlp_t* mlp, const cacto_batch_t* rows_of, int which, void* out,
                        void* stream);  // forward.cu helper (gathered rows)
@@ -606,7 +611,12 @@ extern "C" size_t cacto_loss_workspace_bytes(const cacto_mlp_t* net, int64_t row
   LayerOffsets lo = layer_offsets(shape_of(*net));
   size_t slots = (size_t)num_sms() * (size_t)(lo.total + 1) * es;
   size_t scratch = (size_t)(rows > 0 ? rows : 1) * (2 * CACTO_MAX_IN + 4) * es;  // prep / target / err arrays
-  return ((slots + 255) & ~(size_t)255) + scratch + 256;
+  size_t bytes = ((slots + 255) & ~(size_t)255) + scratch + 256;
+  if (net->head == CACTO_HEAD_LINEAR && critic_tc_eligible(net, nullptr, rows)) {
+    const size_t tcb = critic_tc_workspace_bytes(net, rows);  // tensor-core critic (critic_tc.cu)
+    if (tcb > bytes) bytes = tcb;
+  }
+  return bytes;
 }
 
 static void* scratch_of(const cacto_mlp_t* net, void* ws) {
@@ -692,6 +702,10 @@ extern "C" int cacto_critic_loss(const cacto_mlp_t* critic, const cacto_mlp_t* t
   if (workspace_bytes < cacto_loss_workspace_bytes(critic, batch->rows))
     return set_error(CACTO_EVALUE, "critic_loss: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
+  if (critic_tc_eligible(critic, bootstrap ? target : nullptr, batch->rows)) {
+    *n_partials = 1;
+    return critic_tc_loss(critic, bootstrap ? target : nullptr, batch, k_s, workspace, workspace_bytes, st);
+  }
   if (is_wide(critic)) {
     *n_partials = 1;
     return wide_critic_loss(critic, bootstrap ? target : nullptr, batch, k_s, bootstrap, workspace, workspace_bytes,

@@ -118,7 +118,8 @@ def main():
 
             ms = timed(one, args.steps, torch.cuda.current_stream())
             f = flops_per_sample(H, d)
-            line = {"hidden": H, "batch": B, "path": "simt" if H <= 64 else "tcgen05",
+            line = {"hidden": H, "batch": B,
+                    "path": "tcgen05 layer-wise" if H > 64 else ("tcgen05 fused (critic_tc)" if B >= 8192 else "simt fused"),
                     "ms_per_update": ms, "samples_per_s": B / (ms * 1e-3),
                     "tflops": f * B / (ms * 1e-3) / 1e12, "flops_per_sample": f,
                     "workspace_mb": nbytes / 2 ** 20}
