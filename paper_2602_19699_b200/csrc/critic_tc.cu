@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       if (lane == 0) tc::mbar_arrive(&full_bar);
     };
     auto wait_done = [&]() {
-      tc::mbar_wait_sleep(&done_bar, pd);
+      tc::mbar_wait(&done_bar, pd);
       pd ^= 1;
       tc::tc_fence_after();
     };
@@ -254,15 +254,34 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       const int64_t rr = valid ? a.b.row(gb) : 0;
       float y = 0.f;
       float xin[16];
+      // the owner gathers every per-sample input of the tile up front (one round of
+      // independent loads instead of dependent index -> row chains inside the layer
+      // chain); fixed-trip loops keep the arrays in registers
+      float xr[16], xkr[16], vxr[16], vbar = 0.f;
+      bool gate = false;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) xr[c] = xkr[c] = vxr[c] = 0.f;
+      if (owner && valid) {
+        const float* x = a.b.xa + rr * d;
+        const float* xk = a.b.xa_plus_k + rr * d;
+        const float* vx = a.b.v_bar_x + rr * n;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          if (c < d) {
+            xr[c] = x[c];
+            if (boot) xkr[c] = xk[c];
+          }
+          if (c < n) vxr[c] = vx[c];
+        }
+        vbar = a.b.v_bar[rr];
+        gate = boot && xk[n] < (float)a.b.t_max;
+      }
       // ---- target forward at x_{+k} (nets.py:247-251) --------------------------------
       if (boot) {
         if (owner) {
 #pragma unroll
-          for (int c = 0; c < 16; ++c) xin[c] = 0.f;
-          if (valid) {
-            const float* xk = a.b.xa_plus_k + rr * d;
-            for (int c = 0; c < d; ++c) xin[c] = (xk[c] - a.nc_t.in_center[c]) / a.nc_t.in_half[c];
-          }
+          for (int c = 0; c < 16; ++c)
+            xin[c] = (valid && c < d) ? (xkr[c] - a.nc_t.in_center[c]) * a.nc_t.in_inv_half[c] : 0.f;
         }
         put_input(xin);
         preload_bias(TD, bias_t, 0);
@@ -282,11 +301,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         if (owner) {
           float o[16];
           ld16(TD, o);
-          if (valid) {
-            const float vt = o[0] * (1.f / SO);
-            const bool gate = a.b.xa_plus_k[rr * d + n] < (float)a.b.t_max;
-            y = gate ? vt : 0.f;
-          }
+          if (valid) y = gate ? o[0] * (1.f / SO) : 0.f;
         }
       }
       // ---- critic forward at x, z_i kept in TMEM -------------------------------------
@@ -294,9 +309,9 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
 #pragma unroll
         for (int c = 0; c < 16; ++c) xin[c] = 0.f;
         if (valid) {
-          const float* x = a.b.xa + rr * d;
-          for (int c = 0; c < d; ++c) xin[c] = (x[c] - a.nc.in_center[c]) / a.nc.in_half[c];
-          y += a.b.v_bar[rr];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) xin[c] = c < d ? (xr[c] - a.nc.in_center[c]) * a.nc.in_inv_half[c] : 0.f;
+          y += vbar;
           st16g(a.UA[0] + (B + gb) * 20, xin);  // a_0 = normalised input
           *reinterpret_cast<float4*>(a.UA[0] + (B + gb) * 20 + 16) = make_float4(1.f, 0.f, 0.f, 0.f);
         }
@@ -373,13 +388,15 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           float s0[16];
           ld16(TD, s0);
           if (valid) {
-            const float* vx = a.b.v_bar_x + rr * n;
             float eg2 = 0.f;
             const float coef = -2.f * a.k_s;  // x 1/denom in the reductions
-            for (int c = 0; c < n; ++c) {
-              const float eg = vx[c] - s0[c] * RS / a.nc.in_half[c];
-              eg2 += eg * eg;
-              u0[c] = coef * eg / a.nc.in_half[c];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              if (c < n) {
+                const float eg = vxr[c] - s0[c] * RS * a.nc.in_inv_half[c];
+                eg2 += eg * eg;
+                u0[c] = coef * eg * a.nc.in_inv_half[c];
+              }
             }
             loss_acc += (ev * ev + a.k_s * eg2) * a.inv_denom;
             st16g(a.UA[0] + gb * 20, u0);
@@ -476,7 +493,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     uint32_t pf = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int op = 0; op < nops; ++op) {
-        tc::mbar_wait_sleep(&full_bar, pf);
+        tc::mbar_wait(&full_bar, pf);
         pf ^= 1;
         tc::tc_fence_after();
         const int k = boot ? op : op + 4;  // op index in the full list (targets first)
