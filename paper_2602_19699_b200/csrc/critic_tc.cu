@@ -35,6 +35,8 @@ constexpr int NEPI = 16;  // epilogue warps: 4 per lane quadrant x 16 columns
 constexpr int MMA_WARP = NEPI;
 constexpr int NTHR = NEPI * 32 + 32;
 constexpr uint32_t TD = 0, TA_HI = 64, TA_LO = 96, TZ = 128, TG = 320;
+// the target forward runs before any g_i exists: its D and A live in the G region
+constexpr uint32_t TT_D = TG, TT_AHI = TG + 64, TT_ALO = TG + 96;
 using PL = rtc::Plan<HP>;
 constexpr uint32_t SLOT = PL::SLOT;             // 0 = critic, 1 = target (forward weights)
 constexpr uint32_t W0T = rtc::NOUT * 128;       // W0^T [16][64] (N = padded input width)
@@ -135,7 +137,9 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
   constexpr float RS = 1.f / (S * SB);  // backward product -> value
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full_bar, done_bar;
+  // two layer chains: "c" (critic forward, sweep, gradient and value paths) and
+  // "t" (the target forward, interleaved with the critic forward)
+  __shared__ __align__(8) uint64_t full_bar, done_bar, full_t, done_t;
   __shared__ uint32_t tmem_base_sh;
   __shared__ float red[NTHR / 32];
 
@@ -166,6 +170,8 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
   if (threadIdx.x == 0) {
     tc::mbar_init(&full_bar, NEPI);
     tc::mbar_init(&done_bar, 1);
+    tc::mbar_init(&full_t, NEPI);
+    tc::mbar_init(&done_t, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) tc::tmem_alloc(&tmem_base_sh, 512);
@@ -178,7 +184,6 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
   const int64_t B = a.b.rows;
   const int64_t ntiles = (B + TILE - 1) / TILE;
   const bool boot = a.target != nullptr;
-  const int nops = (boot ? 4 : 0) + 4 + 3 + 3 + 2;
 
   if (warp < NEPI) {
     // ---- epilogue ------------------------------------------------------------------
@@ -189,13 +194,24 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     const bool owner = part == 0;
     const float* w3 = reinterpret_cast<const float*>(base + OFF_W3);
     const uint32_t bias_c = sbase + PL::off_bias, bias_t = sbase + SLOT + PL::off_bias;
-    uint32_t pd = 0;
+    uint32_t pd = 0, pdt = 0;
     float loss_acc = 0.f;
     auto handoff = [&]() {
       tc::tmem_wait_st();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full_bar);
+    };
+    auto handoff_t = [&]() {
+      tc::tmem_wait_st();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full_t);
+    };
+    auto wait_done_t = [&]() {
+      tc::mbar_wait(&done_t, pdt);
+      pdt ^= 1;
+      tc::tc_fence_after();
     };
     auto wait_done = [&]() {
       tc::mbar_wait(&done_bar, pd);
@@ -217,6 +233,18 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       tc::tmem_st8(lrow + TA_HI + (uint32_t)(c0 / 2), hv);
       tc::tmem_st8(lrow + TA_LO + (uint32_t)(c0 / 2), lv);
     };
+    auto put_at = [&](const float (&v)[16]) {  // the target chain's A (in the G region)
+      float hv[8], lv[8];
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) {
+        uint32_t h, l;
+        rtc::split2(v[c], v[c + 1], h, l);
+        hv[c / 2] = __uint_as_float(h);
+        lv[c / 2] = __uint_as_float(l);
+      }
+      tc::tmem_st8(lrow + TT_AHI + (uint32_t)(c0 / 2), hv);
+      tc::tmem_st8(lrow + TT_ALO + (uint32_t)(c0 / 2), lv);
+    };
     auto put_ab = [&](const float (&v)[16]) {  // backward operand, scaled by SB
       float w[16];
 #pragma unroll
@@ -232,7 +260,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       }
       st16(col + (uint32_t)c0, bv);  // my columns of the layer's accumulator
     };
-    auto preload_out_bias = [&](uint32_t bias_s) {  // output layer: D columns 0..15 (part 0)
+    auto preload_out_bias = [&](uint32_t bias_s, uint32_t dcol = TD) {  // output layer: 16 columns (part 0)
       if (!owner) return;
       float bv[16];
 #pragma unroll
@@ -240,12 +268,16 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         const V4<float> v = lds4(bias_s + (uint32_t)((3 * HP + c) * 4), (float*)nullptr);
         bv[c] = v.v[0]; bv[c + 1] = v.v[1]; bv[c + 2] = v.v[2]; bv[c + 3] = v.v[3];
       }
-      st16(TD, bv);
+      st16(dcol, bv);
     };
     // the owner's normalised input row (16 columns) -> A
     auto put_input = [&](const float (&v)[16]) {
       if (!owner) return;
       put_a(v);
+    };
+    auto put_input_t = [&](const float (&v)[16]) {
+      if (!owner) return;
+      put_at(v);
     };
 
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -276,35 +308,18 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         vbar = a.b.v_bar[rr];
         gate = boot && xk[n] < (float)a.b.t_max;
       }
-      // ---- target forward at x_{+k} (nets.py:247-251) --------------------------------
+      // ---- target forward at x_{+k} (nets.py:247-251) and critic forward at x, as two
+      //      interleaved layer chains (z_i of the critic kept in TMEM) -----------------
       if (boot) {
         if (owner) {
 #pragma unroll
           for (int c = 0; c < 16; ++c)
             xin[c] = (valid && c < d) ? (xkr[c] - a.nc_t.in_center[c]) * a.nc_t.in_inv_half[c] : 0.f;
         }
-        put_input(xin);
-        preload_bias(TD, bias_t, 0);
-        handoff();
-        for (int l = 0; l < 3; ++l) {
-          wait_done();
-          float z[16];
-          ld16(TD + c0, z);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) z[c] = AF::apply(z[c]);
-          put_a(z);
-          if (l < 2) preload_bias(TD, bias_t, l + 1);
-          else preload_out_bias(bias_t);
-          handoff();
-        }
-        wait_done();
-        if (owner) {
-          float o[16];
-          ld16(TD, o);
-          if (valid) y = gate ? o[0] * (1.f / SO) : 0.f;
-        }
+        put_input_t(xin);
+        preload_bias(TT_D, bias_t, 0);
+        handoff_t();
       }
-      // ---- critic forward at x, z_i kept in TMEM -------------------------------------
       if (owner) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) xin[c] = 0.f;
@@ -320,6 +335,17 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       preload_bias(TZ, bias_c, 0);
       handoff();
       for (int l = 0; l < 3; ++l) {
+        if (boot) {
+          wait_done_t();
+          float z[16];
+          ld16(TT_D + c0, z);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) z[c] = AF::apply(z[c]);
+          put_at(z);
+          if (l < 2) preload_bias(TT_D, bias_t, l + 1);
+          else preload_out_bias(bias_t, TT_D);
+          handoff_t();
+        }
         wait_done();
         float z[16];
         ld16(TZ + 64 * l + c0, z);
@@ -335,6 +361,14 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         if (l < 2) preload_bias(TZ + 64 * (l + 1), bias_c, l + 1);
         else preload_out_bias(bias_c);
         handoff();
+      }
+      if (boot) {
+        wait_done_t();
+        if (owner) {
+          float o[16];
+          ld16(TT_D, o);
+          if (valid) y += gate ? o[0] * (1.f / SO) : 0.f;
+        }
       }
       // output: V, e_v, delta; then the sweep starts: g_2 = act'(z_2) w_3
       wait_done();
@@ -490,23 +524,36 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     const uint32_t i64 = tc::idesc_f16(HP), i16 = tc::idesc_f16(rtc::NOUT);
     auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
     const uint32_t ahi = tmem + TA_HI, alo = tmem + TA_LO;
-    uint32_t pf = 0;
+    uint32_t pf = 0, pft = 0;
+    auto fwd = [&](uint32_t so, int l, uint32_t dcol, uint32_t ah, uint32_t al) {
+      if (l == 0) issue<1>(dcol, ah, al, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), i64, false);
+      else if (l < 3)
+        issue<4>(dcol, ah, al, desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH),
+                 desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH + PL::WH), i64, false);
+      else issue<4>(dcol, ah, al, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), i16, false);
+    };
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      for (int op = 0; op < nops; ++op) {
+      for (int l = 0; l < 4; ++l) {  // forwards: target layer l, then critic layer l
+        if (boot) {
+          tc::mbar_wait(&full_t, pft);
+          pft ^= 1;
+          tc::tc_fence_after();
+          fwd(SLOT, l, tmem + TT_D, tmem + TT_AHI, tmem + TT_ALO);
+          tc::tc_commit_elect(&done_t);
+          __syncwarp();
+        }
         tc::mbar_wait(&full_bar, pf);
         pf ^= 1;
         tc::tc_fence_after();
-        const int k = boot ? op : op + 4;  // op index in the full list (targets first)
-        if (k < 8) {  // forward layers: target (k < 4) or critic (4 <= k < 8)
-          const uint32_t so = k < 4 ? SLOT : 0u;
-          const int l = k & 3;
-          const uint32_t dcol = (k >= 4 && l < 3) ? tmem + TZ + 64 * l : tmem + TD;
-          if (l == 0) issue<1>(dcol, ahi, alo, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), i64, false);
-          else if (l < 3)
-            issue<4>(dcol, ahi, alo, desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH),
-                     desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH + PL::WH), i64, false);
-          else issue<4>(dcol, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), i16, false);
-        } else if (k == 8) {
+        fwd(0, l, l < 3 ? tmem + TZ + 64 * l : tmem + TD, ahi, alo);
+        tc::tc_commit_elect(&done_bar);
+        __syncwarp();
+      }
+      for (int k = 8; k < 16; ++k) {  // sweep, gradient path, value path
+        tc::mbar_wait(&full_bar, pf);
+        pf ^= 1;
+        tc::tc_fence_after();
+        if (k == 8) {
           issue<4>(tmem + TD, ahi, alo, desc(OFF_W2T), desc(OFF_W2T + WHT), i64, true);  // s_2
         } else if (k == 9) {
           issue<4>(tmem + TD, ahi, alo, desc(OFF_W1T), desc(OFF_W1T + WHT), i64, true);  // s_1
