@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
 #pragma unroll
           for (int c = 0; c < CH; c += 2) {
             uint32_t h, lo;
-            split2(AF::apply(z[c]), AF::apply(z[c + 1]), h, lo);
+            if constexpr (ACT == CACTO_ACT_ELU) elu_split2(z[c], z[c + 1], AF::S, h, lo);
+            else split2(AF::apply(z[c]), AF::apply(z[c + 1]), h, lo);
             hv[c / 2] = __uint_as_float(h);
             lv[c / 2] = __uint_as_float(lo);
           }

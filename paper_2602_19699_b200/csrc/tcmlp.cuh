@@ -57,6 +57,34 @@ CACTO_D void split2(float v0, float v1, uint32_t& hi, uint32_t& lo) {
   lo = pack_h2(v0 - hf.x, v1 - hf.y);
 }
 
+// ---- packed fp32x2 arithmetic (sm_100: one instruction for two lanes' worth) ----
+CACTO_D uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+CACTO_D void f2unpack(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+CACTO_D uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+CACTO_D uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+CACTO_D uint64_t f2sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+CACTO_D uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 // stage W (row-major [rows][cols], stride) * scale as hi/lo fp16 K-major SW128
 // operands of rrows x kcols (zero padded); kcols <= 64
 CACTO_D void stage_w(unsigned char* hi, unsigned char* lo, const float* src, int rows, int cols, int stride,
@@ -101,6 +129,28 @@ CACTO_D void issue_layer(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, u
 }
 
 }  // namespace rtc
+
+// ELU of an accumulator pair D = S z and its 3xFP16 split, on packed fp32x2
+// arithmetic: ELU(z) = max(D,0)/S + (ex2(min(D,0)/8) - 1)
+template <int ACT>
+struct ActTC;
+
+CACTO_D void elu_split2(float d0, float d1, float S, uint32_t& hi, uint32_t& lo) {
+  using namespace rtc;
+  const uint64_t m = f2mul(f2pack(fminf(d0, 0.f), fminf(d1, 0.f)), f2pack(1.f / rtc::WSCALE, 1.f / rtc::WSCALE));
+  float m0, m1;
+  f2unpack(m, m0, m1);
+  const uint64_t e = f2add(f2pack(tc::ex2_ftz(m0), tc::ex2_ftz(m1)), f2pack(-1.f, -1.f));
+  const uint64_t v = f2fma(f2pack(fmaxf(d0, 0.f), fmaxf(d1, 0.f)), f2pack(1.f / S, 1.f / S), e);
+  float v0, v1;
+  f2unpack(v, v0, v1);
+  __half2 h = __floats2half2_rn(v0, v1);
+  const float2 hf = __half22float2(h);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  float l0, l1;
+  f2unpack(f2sub(v, f2pack(hf.x, hf.y)), l0, l1);
+  lo = rtc::pack_h2(l0, l1);
+}
 
 template <int ACT>
 struct ActTC {
