@@ -309,20 +309,17 @@ def main():
         if world == 1:
             out = pipe.run(x0, keep_global)
             return out["order"], out["U"]
-        out = pipe.run(x0, min(keep_global, N), warm_starts=False)
-        # shard winners -> one all-gather -> exact merge (identical on every rank)
+        # every global winner is among its own shard's top-keep, so each rank keeps the
+        # warm starts of its local top-keep (taken from its cost rollout) and, after the
+        # exact merge, a mask of which of them made the global cut -- no second rollout
+        # and no control traffic between ranks
+        out = pipe.run(x0, min(keep_global, N), warm_starts=True)
         rs, ro, rx = parallel.gather_winners(out["scores"], out["order"] + base,
                                              x0.index_select(0, out["order"]), keep_global)
         pos = parallel.merge_positions(rs, ro, keep_global, parallel.device_merge)
-        gorder, gx = ro.index_select(0, pos), rx.index_select(0, pos)
-        lo, hi = parallel.shard_range(keep_global, rank, world)
-        mine = gx[lo:hi].contiguous()
-        U = torch.empty((hi - lo, T, spec.m), device="cuda", dtype=torch.float32 if args.precision == "fp32"
-                        else torch.float64)
-        if hi > lo:
-            _lib.call("cacto_rollout", pipe.sysd, None, pipe.actor.desc, mine.data_ptr(), None, 0, hi - lo, T,
-                      U.data_ptr(), None, None, None, stream)
-        return gorder, U
+        gorder = ro.index_select(0, pos)
+        kept = torch.isin(out["order"] + base, gorder)
+        return gorder, (out["U"], kept)
 
     def timed(fn, K, W):
         for _ in range(W):
@@ -358,22 +355,26 @@ def main():
     launches_per_step = pipe.kernel_launches
 
     # ---- e2e through the public API: pinned host -> device -> kept order + U back --
-    keep_local_U = keep_global if world == 1 else parallel.shard_range(keep_global, rank, world)[1] - \
-        parallel.shard_range(keep_global, rank, world)[0]
+    keep_local_U = keep_global if world == 1 else min(keep_global, N)
     esz = 4 if args.precision == "fp32" else 8
     order_host = torch.empty(keep_global, dtype=torch.int64).pin_memory()
     U_host = torch.empty((keep_local_U, T, spec.m), dtype=torch.float32 if esz == 4 else torch.float64).pin_memory()
+    mask_host = torch.empty(keep_local_U, dtype=torch.bool).pin_memory()
 
     def e2e_step():
         xd = x0_pinned.to("cuda", non_blocking=True)
         order, U = step(xd)
         order_host.copy_(order, non_blocking=True)
-        U_host.copy_(U, non_blocking=True)
+        if world == 1:
+            U_host.copy_(U, non_blocking=True)
+        else:
+            U_host.copy_(U[0], non_blocking=True)
+            mask_host.copy_(U[1], non_blocking=True)
 
     e2e_ms = timed(e2e_step, args.steps, args.warmup)
     e2e_value = (N * world) / (e2e_ms * 1e-3)
     h2d = N * spec.n * 8
-    d2h = keep_global * 8 + keep_local_U * T * spec.m * esz
+    d2h = keep_global * 8 + keep_local_U * T * spec.m * esz + (keep_local_U if world > 1 else 0)
 
     # ---- roofline of the dominant kernel (K1 rollout over all candidates) ---------
     x0r = x0_dev
