@@ -210,6 +210,34 @@ int cacto_ring_push(const cacto_batch_t* src, void* ring_xa, void* ring_u, void*
                     void* ring_v_bar_x, void* ring_xa_plus_k, int64_t capacity, int64_t cursor,
                     void* stream);
 
+/* -- (8f row 1) replay producer: ilqr.kstep_targets (ilqr.py:358-407, without a
+ * critic hook -- the trainer's call, trainer.py:200-201) of a batch of solutions
+ * + ReplayBuffer.push_many (buffer.py:108-130), one launch.
+ * Solutions are concatenated row-wise (float64, device): solution r owns rows
+ * [offsets[r], offsets[r+1]) = its T_r + 1 time steps; X / step_costs / v_bar /
+ * v_bar_x hold all T_r + 1 rows (Trajectory.X, .step_costs, SolveResult.V_bar,
+ * .V_bar_x, ilqr.py:59-94), U holds T_r rows plus one ignored padding row. */
+typedef struct cacto_solutions {
+  int32_t n, m;
+  int64_t count;            /* R solutions                                   */
+  int64_t rows;             /* offsets[R] = sum (T_r + 1)                     */
+  const int64_t* offsets;   /* [R + 1]                                       */
+  const int32_t* t0;        /* [R]   time index of X[0] (Trajectory.t0)       */
+  const double* X;          /* [rows, n] */
+  const double* U;          /* [rows, m] */
+  const double* step_costs; /* [rows]    */
+  const double* v_bar;      /* [rows]    */
+  const double* v_bar_x;    /* [rows, n] */
+} cacto_solutions_t;
+/* Writes concatenated target row i (i >= first; earlier rows are the ones FIFO
+ * eviction drops, buffer.py:118-121: first = max(0, rows - capacity)) to ring row
+ * (cursor + i - first) % capacity, in the ring's dtype.  K < 1 -> CACTO_EVALUE
+ * (ilqr.py:371-372).  *bad (device int32, caller-zeroed) is set to 1 when a
+ * v_bar is not finite (the reference's TOSample raises ValueError, buffer.py:33-35). */
+int cacto_kstep_push(const cacto_solutions_t* solutions, int32_t K, int32_t ring_dtype, void* ring_xa,
+                     void* ring_u, void* ring_v_bar, void* ring_v_bar_x, void* ring_xa_plus_k,
+                     int64_t capacity, int64_t cursor, int64_t first, int32_t* bad, void* stream);
+
 /* -- (a9-a13) fused losses ---------------------------------------------------
  * Each writes per-CTA partial sums into `workspace`; `cacto_reduce_grads`
  * (or the fused `cacto_reduce_adam`) folds them.  Gradients are in the padded

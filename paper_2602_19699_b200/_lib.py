@@ -60,6 +60,13 @@ class CactoBatch(ctypes.Structure):
                 ("cycle", ctypes.c_void_p), ("idx_stride", ctypes.c_int64)]
 
 
+class CactoSolutions(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("count", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("offsets", ctypes.c_void_p), ("t0", ctypes.c_void_p), ("X", ctypes.c_void_p),
+                ("U", ctypes.c_void_p), ("step_costs", ctypes.c_void_p), ("v_bar", ctypes.c_void_p),
+                ("v_bar_x", ctypes.c_void_p)]
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -94,6 +101,8 @@ SIGNATURES = {
     "cacto_select_merge": (ctypes.c_int, [_I32, _P, _P, _I32, _I64, _P, _P, _P, _SZ, _P]),
     "cacto_gather": (ctypes.c_int, [_PBATCH, _P, _P, _P, _P, _P, _P]),
     "cacto_ring_push": (ctypes.c_int, [_PBATCH, _P, _P, _P, _P, _P, _I64, _I64, _P]),
+    "cacto_kstep_push": (ctypes.c_int, [ctypes.POINTER(CactoSolutions), _I32, _I32, _P, _P, _P, _P, _P, _I64, _I64,
+                                         _I64, _P, _P]),
     "cacto_loss_workspace_bytes": (_SZ, [_PMLP, _I64]),
     "cacto_critic_loss": (ctypes.c_int, [_PMLP, _PMLP, _PBATCH, _D, _I32, _P, _SZ, _PI32, _P]),
     "cacto_actor_loss": (ctypes.c_int, [_PMLP, _PMLP, _PSYS, _PCOST, _PBATCH, _P, _P, _SZ, _PI32, _P]),

@@ -175,7 +175,11 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       if (lane == 0) tc::mbar_arrive(&full_bar[g]);
     };
     auto wait_done = [&]() {
+#ifdef CACTO_RTC_PLAIN_WAIT
+      tc::mbar_wait(&done_bar[g], pd);
+#else
       tc::mbar_wait_sleep(&done_bar[g], pd);
+#endif
       pd ^= 1;
       tc::tc_fence_after();
     };

@@ -2,8 +2,8 @@
 `trajrl.trainer.run_iteration`, trainer.py:168-255).
 
 Same control flow and the same random streams as the reference; the TO solve
-(`solve_batch`), the k-step targets and the reports stay on the reference's CPU
-code, while
+(`solve_batch`) and the reports stay on the reference's CPU code, while
+  * k-step targets + replay push (the producer)    -> cacto_kstep_push (200-201)
   * BIC candidate scoring + stable selection      -> K2/K3 (trainer.py:183-186)
   * warm-start actor rollouts of the kept starts   -> K1, one batched launch (192-193)
   * the M critic/actor + M std update cycles       -> UpdateEngine graphs (208-234)
@@ -50,6 +50,7 @@ def _engine(state):
                            lr_actor=cfg.lr_actor, lr_critic=cfg.lr_critic, lr_std=cfg.lr_std,
                            adam_states=(state.adam_actor, state.adam_critic, state.adam_std))
         state._cacto_engine = eng
+        state.buffer = dbuf  # same API as the reference ring (push_many / sample_minibatch / dump)
     return eng
 
 
@@ -99,10 +100,9 @@ def run_iteration(state, iter_idx: int, trajrl):
         raise RuntimeError("iteration cap not resolved; run via train()")
 
     results = T.solve_batch(model, fld, starts, warms, max_iter, state.reg, cfg.tol, cfg.workers)
-    for res in results:
-        samples = T.kstep_targets(res, cfg.k_lookahead)
-        state.buffer.push_many(samples)
-        eng.buffer.push_many(samples)
+    # replay producer on the device: k-step targets of every solution + FIFO push,
+    # one H2D copy and one launch (trainer.py:200-201); state.buffer is the device ring
+    eng.buffer.push_kstep(results, cfg.k_lookahead)
     state.episodes_cum += len(results)
     costs = np.array([r.cost for r in results])
     conv = float(np.mean([r.converged for r in results]))

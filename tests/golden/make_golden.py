@@ -2,7 +2,7 @@
 
 Run in the build container (where /root/reference exists), never on the GPU box:
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [fixture ...]
 
 It imports `trajrl` read-only from /root/reference/pkg/src, evaluates the hot
 path functions on seeded inputs and writes `tests/golden/*.npz`.  The fixtures
@@ -26,7 +26,7 @@ sys.path.insert(0, str(REF / "src"))
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parents[1]))
 
-from trajrl import envs as R_envs, nets as R_nets, trainer as R_trainer  # noqa: E402
+from trajrl import envs as R_envs, ilqr as R_ilqr, nets as R_nets, trainer as R_trainer  # noqa: E402
 from trajrl.buffer import ReplayBuffer, SampleBatch, TOSample  # noqa: E402
 from trajrl.config import load_config  # noqa: E402
 from trajrl.envs import TimeState  # noqa: E402
@@ -363,11 +363,66 @@ def make_sampling(cfgs):
     return data
 
 
+def _solution_dict(prefix, res):
+    tr = res.traj
+    return {f"{prefix}_X": tr.X, f"{prefix}_U": tr.U, f"{prefix}_sc": tr.step_costs,
+            f"{prefix}_t0": np.array(tr.t0), f"{prefix}_Vb": np.asarray(res.V_bar, float),
+            f"{prefix}_Vbx": np.asarray(res.V_bar_x, float)}
+
+
+def make_kstep(cfgs):
+    """Replay producer: kstep_targets (ilqr.py:358-407) on real
+    iLQR solutions (pointmass, dubins; t0 = 0 and t0 > 0) and on synthetic
+    solutions with long horizons (windows past NumPy's 128-term pairwise block),
+    each pushed through ReplayBuffer.push_many into a small ring that wraps, and
+    the TRLB dump of that ring (buffer.py:142-152)."""
+    from trajrl.ilqr import SolveResult, Trajectory, solve_batch
+    import tempfile
+    from types import SimpleNamespace
+    data = {}
+    results = {}
+    for name in ("pointmass", "dubins"):
+        spec, fld = cfgs[name]
+        st = R_envs.sample_initial_states(spec, 3, 11, R_envs.Region.WORKSPACE)
+        st = [st[0], TimeState(st[1].x, 7), TimeState(st[2].x, spec.t_max - 3)]
+        warms = [np.zeros((spec.t_max - s.t, spec.m)) for s in st]
+        results[name] = (spec, solve_batch(spec, fld, st, warms, 4))
+    rng = np.random.default_rng(21)
+    syn = []
+    for T, t0 in ((150, 0), (9, 2), (1, 0), (300, 5)):
+        n, m = 3, 2
+        tr = Trajectory(rng.normal(size=(T + 1, n)), rng.normal(size=(T, m)), rng.normal(size=T + 1) ** 2 * 10, t0)
+        syn.append(SolveResult(tr, tr.cost, np.cumsum(rng.normal(size=T + 1)), rng.normal(size=(T + 1, n)), 1, True,
+                               model=SimpleNamespace(m=m)))
+    results["synthetic"] = (None, syn)
+    for name, (spec, res) in results.items():
+        data[f"ks_{name}_count"] = np.array(len(res))
+        for i, r in enumerate(res):
+            data.update(_solution_dict(f"ks_{name}_{i}", r))
+        Ks = (1, 4, 10, 140, 400) if name == "synthetic" else (1, 5, 10, 1000)
+        data[f"ks_{name}_Ks"] = np.array(Ks)
+        for K in Ks:
+            rows = [s for r in res for s in R_ilqr.kstep_targets(r, K)]
+            data.update(batch_dict(f"ks_{name}_K{K}", SampleBatch.from_samples(rows, 0)))
+        n, m = res[0].traj.X.shape[1], res[0].traj.U.shape[1]
+        cap = 37
+        buf = ReplayBuffer(n=n, m=m, t_max=0, capacity=cap, model_name=name, k_lookahead=10)
+        for r in res:
+            buf.push_many(R_ilqr.kstep_targets(r, 10))
+        with tempfile.TemporaryDirectory() as td:
+            buf.dump(Path(td) / "b.trlb")
+            data[f"ks_{name}_dump"] = np.frombuffer((Path(td) / "b.trlb").read_bytes(), dtype=np.uint8)
+        data[f"ks_{name}_cap"] = np.array(cap)
+    return data
+
+
 def main():
     cfgs = configs()
-    out = {"rollout": make_rollouts(cfgs), "nets": make_nets(), "losses": make_losses(cfgs),
-           "optim": make_optim(), "select": make_select(cfgs), "buffer": make_buffer(),
-           "sampling": make_sampling(cfgs)}
+    only = sys.argv[1:]
+    builders = {"rollout": lambda: make_rollouts(cfgs), "nets": make_nets, "losses": lambda: make_losses(cfgs),
+                "optim": make_optim, "select": lambda: make_select(cfgs), "buffer": make_buffer,
+                "sampling": lambda: make_sampling(cfgs), "kstep": lambda: make_kstep(cfgs)}
+    out = {name: fn() for name, fn in builders.items() if not only or name in only}
     for name, data in out.items():
         np.savez_compressed(HERE / f"{name}.npz", **data)
         print(name, len(data), "arrays", (HERE / f"{name}.npz").stat().st_size, "bytes")

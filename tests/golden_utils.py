@@ -113,3 +113,17 @@ def batch(data, prefix):
 
 
 SYSTEMS = ("toy1d", "pointmass", "dubins", "manipulator3", "aliengo_lipm")
+
+
+KSTEP_SETS = ("pointmass", "dubins", "synthetic")
+
+
+def solutions(d, name):
+    """The iLQR solutions of a kstep fixture set, as reference-shaped objects
+    (`SolveResult` with `.traj.X/.U/.step_costs/.t0`, `.V_bar`, `.V_bar_x`)."""
+    out = []
+    for i in range(int(d[f"ks_{name}_count"])):
+        p = f"ks_{name}_{i}"
+        traj = SimpleNamespace(X=d[f"{p}_X"], U=d[f"{p}_U"], step_costs=d[f"{p}_sc"], t0=int(d[f"{p}_t0"]))
+        out.append(SimpleNamespace(traj=traj, V_bar=d[f"{p}_Vb"], V_bar_x=d[f"{p}_Vbx"]))
+    return out

@@ -210,3 +210,39 @@ def test_lemire_replay_matches_generator():
     raws = O_rng.raw_stream(seed, 64)
     idx = O_rng.lemire_indices(raws, 50, 64)
     np.testing.assert_array_equal(idx, np.random.default_rng(seed).integers(0, 50, 64))
+
+
+# -- replay producer: kstep_targets + push_many + TRLB dump -------
+
+@pytest.mark.parametrize("name", G.KSTEP_SETS)
+def test_kstep_rows_bitwise(name):
+    d = G.load("kstep")
+    sols = G.solutions(d, name)
+    for K in d[f"ks_{name}_Ks"]:
+        got = O_buffer.concat_rows([O_buffer.kstep_rows(s.traj.X, s.traj.U, s.traj.step_costs, s.traj.t0,
+                                                        s.V_bar, s.V_bar_x, int(K)) for s in sols])
+        ref = G.batch(d, f"ks_{name}_K{K}")
+        for k in O_buffer.COLUMNS:
+            np.testing.assert_array_equal(got[k], getattr(ref, k), err_msg=f"K={K} {k}")
+
+
+@pytest.mark.parametrize("name", G.KSTEP_SETS)
+def test_kstep_ring_dump_bitwise(name):
+    d = G.load("kstep")
+    sols = G.solutions(d, name)
+    n, m = sols[0].traj.X.shape[1], sols[0].traj.U.shape[1]
+    ring = O_buffer.Ring(n, m, int(d[f"ks_{name}_cap"]))
+    for s in sols:
+        ring.push_many(O_buffer.kstep_rows(s.traj.X, s.traj.U, s.traj.step_costs, s.traj.t0, s.V_bar, s.V_bar_x, 10))
+    blob = O_buffer.dump_bytes(ring, name, 10)
+    assert blob == d[f"ks_{name}_dump"].tobytes()
+    got_name, gn, gm, gk, rows = O_buffer.parse_dump(blob)
+    assert (got_name, gn, gm, gk) == (name, n, m, 10)
+    assert rows["v_bar"].shape[0] == ring.size
+
+
+def test_kstep_rejects_bad_window():
+    with pytest.raises(ValueError):
+        O_buffer.kstep_rows(np.zeros((3, 2)), np.zeros((2, 1)), np.zeros(3), 0, np.zeros(3), np.zeros((3, 2)), 0)
+    with pytest.raises(ValueError):
+        O_buffer.parse_dump(b"XXXX" + bytes(40))
