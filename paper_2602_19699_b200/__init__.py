@@ -19,11 +19,16 @@ def library_path():
     return str(_lib.LIB_PATH)
 
 
-def install(trajrl_module):
+def install(trajrl_module, iteration: bool = True):
     """Rebind the reference's hot-path functions onto the B200 implementation:
     trajrl.nets.{mlp_forward, critic_loss, actor_loss, std_critic_loss,
     adam_step, polyak, actor_rollout} and trajrl.trainer.select_initial_states_bic
-    (call sites trainer.py:186, 192-193, 211-233, 267-268)."""
+    (call sites trainer.py:186, 192-193, 211-233, 267-268), and -- with
+    `iteration=True` (default) -- trajrl.trainer.run_iteration (trainer.py:168-255)
+    by the batched device iteration (iteration.run_iteration: one launch per
+    phase, the replay producer, the CUDA-graph update engine), so
+    `trajrl.trainer.train` runs the whole hot path on the B200.  Returns
+    `uninstall()`."""
     from . import nets, trainer
     tn = trajrl_module.nets
     tt = trajrl_module.trainer
@@ -49,6 +54,9 @@ def install(trajrl_module):
     swap(tn, "adam_step", adam_step)
     swap(tn, "actor_rollout", actor_rollout)
     swap(tt, "select_initial_states_bic", trainer.select_initial_states_bic)
+    if iteration:
+        from . import iteration as _it
+        swap(tt, "run_iteration", lambda state, iter_idx: _it.run_iteration(state, iter_idx, trajrl_module))
 
     def uninstall():
         for (mod, name), fn in saved.items():

@@ -194,27 +194,31 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       const int slot = P < n_pre ? P + 1 : 0;
       for (int l = 0; l < nh; ++l) {  // hidden layers
         wait_done();
+        // 16-column chunks, software pipelined: the next chunk's tcgen05.ld is in
+        // flight while this chunk's activations are computed and stored (a single
+        // warp's ld + wait costs ~160 cycles, profiles/probe_tmem.cu)
+        float za[16], zb[16];
+        tc::tmem_ld16(t_d + (uint32_t)c_base, za);
+        tc::tmem_wait_ld_dep(za);
 #pragma unroll
-        for (int c0 = 0; c0 < COLS; c0 += 32) {
-          constexpr int CH = COLS < 32 ? COLS : 32;
-          float z[CH], hv[CH / 2], lv[CH / 2];
-          if constexpr (CH == 32) tc::tmem_ld32_wait(t_d + (uint32_t)(c_base + c0), z);
-          else tc::tmem_ld16_wait(t_d + (uint32_t)(c_base + c0), z);
+        for (int c0 = 0; c0 < COLS; c0 += 16) {
+          if (c0 + 16 < COLS) tc::tmem_ld16(t_d + (uint32_t)(c_base + c0 + 16), zb);
+          float hv[8], lv[8];
 #pragma unroll
-          for (int c = 0; c < CH; c += 2) {
+          for (int c = 0; c < 16; c += 2) {
             uint32_t h, lo;
-            if constexpr (ACT == CACTO_ACT_ELU) elu_split2(z[c], z[c + 1], AF::S, h, lo);
-            else split2(AF::apply(z[c]), AF::apply(z[c + 1]), h, lo);
+            if constexpr (ACT == CACTO_ACT_ELU) elu_split2(za[c], za[c + 1], AF::S, h, lo);
+            else split2(AF::apply(za[c]), AF::apply(za[c + 1]), h, lo);
             hv[c / 2] = __uint_as_float(h);
             lv[c / 2] = __uint_as_float(lo);
           }
           const uint32_t ac = (uint32_t)((c_base + c0) / 2);
-          if constexpr (CH == 32) {
-            tc::tmem_st16(t_ahi + ac, hv);
-            tc::tmem_st16(t_alo + ac, lv);
-          } else {
-            tc::tmem_st8(t_ahi + ac, hv);
-            tc::tmem_st8(t_alo + ac, lv);
+          tc::tmem_st8(t_ahi + ac, hv);
+          tc::tmem_st8(t_alo + ac, lv);
+          if (c0 + 16 < COLS) {
+            tc::tmem_wait_ld_dep(zb);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) za[c] = zb[c];
           }
         }
         preload_bias(slot, l + 1);

@@ -228,6 +228,15 @@ CACTO_D void mma_tf32_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, ui
       : "memory");
 }
 CACTO_D void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait::ld that also ties the registers of an outstanding tmem_ld16 to it, so no
+// consumer of v can be scheduled before the load has landed (software pipelining)
+CACTO_D void tmem_wait_ld_dep(float (&v)[16]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])::"memory");
+}
 // the TF32 "lo" part of x (the tensor core reads x's upper 19 bits as hi)
 CACTO_D float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 // round-to-nearest TF32 split: x = hi + lo with |lo| <= 2^-12 |x| (half the

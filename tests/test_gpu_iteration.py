@@ -90,3 +90,28 @@ def test_iteration_matches_reference():
     np.testing.assert_allclose(g2.to_cost_mean, r2.to_cost_mean, rtol=1e-6)
     np.testing.assert_allclose(g2.critic_loss_mean, r2.critic_loss_mean, rtol=1e-6)
     np.testing.assert_allclose(g2.std_loss_mean, r2.std_loss_mean, rtol=1e-6)
+
+
+def test_installed_train_matches_reference():
+    # `install(trajrl)` rebinds the reference's hot functions and run_iteration;
+    # trajrl.trainer.train (trainer.py:283-330: calibration, iterations, the
+    # actor-warm-start calibration after iteration 1) then runs on the B200
+    cfg = small_cfg()
+    from dataclasses import replace
+    cfg = replace(cfg, max_iter_first=None, max_iter_later=None, calibration_probes=10, calibration_cap=8)
+    a_ref, c_ref, s_ref, reps_ref = T.train(cfg)
+    uninstall = P.install(trajrl)
+    try:
+        a_gpu, c_gpu, s_gpu, reps_gpu = T.train(cfg)
+    finally:
+        uninstall()
+    assert T.run_iteration is not None and T.run_iteration.__module__ == "trajrl.trainer"
+    assert len(reps_gpu) == len(reps_ref) == cfg.iterations
+    r1, g1 = reps_ref[0], reps_gpu[0]
+    assert g1.to_cost_mean == r1.to_cost_mean   # naive warm starts: identical TO solutions
+    for r, g in zip(reps_ref, reps_gpu):
+        np.testing.assert_allclose(g.to_cost_mean, r.to_cost_mean, rtol=1e-6)
+        np.testing.assert_allclose(g.critic_loss_mean, r.critic_loss_mean, rtol=1e-6)
+        np.testing.assert_allclose(g.std_loss_mean, r.std_loss_mean, rtol=1e-6)
+    for a, b in zip(a_gpu.weights + c_gpu.weights + s_gpu.weights, a_ref.weights + c_ref.weights + s_ref.weights):
+        np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-8)
