@@ -59,12 +59,14 @@ def test_struct_layout_matches_c(tmp_path):
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "cacto_b200.h"\n'
                    'int main(){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(cacto_mlp_t), '
                    'offsetof(cacto_mlp_t, params), sizeof(cacto_system_t), sizeof(cacto_cost_t), '
-                   'sizeof(cacto_batch_t), offsetof(cacto_batch_t, xa_plus_k));return 0;}\n')
+                   'sizeof(cacto_batch_t), offsetof(cacto_batch_t, xa_plus_k));'
+                   'printf("%zu %zu\\n", sizeof(cacto_solutions_t), offsetof(cacto_solutions_t, v_bar_x));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     want = [ctypes.sizeof(lib.CactoMlp), lib.CactoMlp.params.offset, ctypes.sizeof(lib.CactoSystem),
-            ctypes.sizeof(lib.CactoCost), ctypes.sizeof(lib.CactoBatch), lib.CactoBatch.xa_plus_k.offset]
+            ctypes.sizeof(lib.CactoCost), ctypes.sizeof(lib.CactoBatch), lib.CactoBatch.xa_plus_k.offset,
+            ctypes.sizeof(lib.CactoSolutions), lib.CactoSolutions.v_bar_x.offset]
     assert got == want
 
 
