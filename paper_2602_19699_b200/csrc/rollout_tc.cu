@@ -285,15 +285,17 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
           pf[t] ^= 1;
           tc::tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(t * TM::PER_TILE), ahi = d + HP, alo = d + HP + HP / 2;
+          const uint32_t bar = saddr(&done_bar[t]);
           if (l == 0) {
-            issue_layer<KIN / 16>(d, ahi, alo, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), idesc_h);
+            issue_layer_commit<KIN / 16>(d, ahi, alo, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), idesc_h,
+                                         bar);
           } else if (l < nh) {
             const uint32_t wo = so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;
-            issue_layer<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h);
+            issue_layer_commit<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h, bar);
           } else {
-            issue_layer<HP / 16>(d, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), idesc_o);
+            issue_layer_commit<HP / 16>(d, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), idesc_o,
+                                        bar);
           }
-          tc::tc_commit_elect(&done_bar[t]);
           __syncwarp();
         }
       }

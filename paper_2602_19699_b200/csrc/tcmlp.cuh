@@ -140,6 +140,76 @@ CACTO_D void issue_layer(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, u
   }
 }
 
+// one layer of one tile + its commit in ONE asm statement: a single elect.sync,
+// the 3 * KSTEPS MMAs (k-step offsets added in PTX) and the commit -- the issuing
+// warp shares its scheduler with four busy epilogue warps, so every instruction on
+// this path delays the tile (a per-MMA elect + descriptor moves cost ~700 cycles
+// per layer, measured with a clock64 timeline)
+template <int KSTEPS>
+CACTO_D void issue_layer_commit(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
+                                uint32_t bar);
+template <>
+CACTO_D void issue_layer_commit<1>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
+                                   uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "setp.eq.u32 p, 1, 1;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar)
+      : "memory");
+}
+template <>
+CACTO_D void issue_layer_commit<2>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
+                                   uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "setp.eq.u32 p, 1, 1;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "add.u32 ah, %1, 8;\n\tadd.u32 al, %2, 8;\n\tadd.u64 bh, %3, 2;\n\tadd.u64 bl, %4, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar)
+      : "memory");
+}
+template <>
+CACTO_D void issue_layer_commit<4>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
+                                   uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "setp.eq.u32 p, 1, 1;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "add.u32 ah, %1, 8;\n\tadd.u32 al, %2, 8;\n\tadd.u64 bh, %3, 2;\n\tadd.u64 bl, %4, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "add.u32 ah, %1, 16;\n\tadd.u32 al, %2, 16;\n\tadd.u64 bh, %3, 4;\n\tadd.u64 bl, %4, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "add.u32 ah, %1, 24;\n\tadd.u32 al, %2, 24;\n\tadd.u64 bh, %3, 6;\n\tadd.u64 bl, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar)
+      : "memory");
+}
+
 }  // namespace rtc
 
 // ELU of an accumulator pair D = S z and its 3xFP16 split, on packed fp32x2
