@@ -92,4 +92,50 @@ struct PairwiseSum {
   }
 };
 
+// The same summation with the 8 partial sums in shared memory (one 9-float
+// stride per thread, bank-conflict free): the tensor-core rollout keeps its
+// registers for the epilogue, and a dynamically indexed r[i & 7] is one LDS/STS
+// instead of an 8-way select chain.
+template <typename T>
+struct PairwiseSumS {
+  T* r;
+  T res;
+  int n;
+  CACTO_D void init(int n_, T* r_) {
+    n = n_;
+    r = r_;
+    res = T(0);
+  }
+  CACTO_D T combine() const {
+    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  }
+  CACTO_D void add(int i, T v) {
+    if (n < 8) {
+      res += v;
+      return;
+    }
+    if (n > 128) {  // chained blocks of 128, as PairwiseSum
+      const int blk = i >> 7, off = i & 127;
+      sub(off, min(128, n - (blk << 7)), v, blk > 0);
+      return;
+    }
+    sub(i, n, v, false);
+  }
+  CACTO_D void sub(int i, int len, T v, bool chain) {
+    const int body = len - (len % 8);
+    if (len < 8) {
+      res += v;
+      return;
+    }
+    if (i < body) {
+      const int j = i & 7;
+      r[j] = (i < 8) ? v : r[j] + v;
+      if (i == body - 1 && body == len) res = chain ? res + combine() : combine();
+    } else {
+      if (i == body) res = chain ? res + combine() : combine();
+      res += v;
+    }
+  }
+};
+
 }  // namespace cacto

@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   const bool owner = epi && part == 0 && gi < a.N;
   float x[n];
   int t0 = 0, T_i = 0;
-  PairwiseSum<float> acc;
+  PairwiseSumS<float> acc;
+  // per-thread pairwise partial sums live after the network slots
+  float* acc_s = (float*)(base + (1 + n_pre) * PL::SLOT) + threadIdx.x * 9;
 #pragma unroll
   for (int c = 0; c < n; ++c) x[c] = 0.f;
   if (owner) {
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     for (int c = 0; c < n; ++c) x[c] = (float)a.x0[gi * n + c];
     t0 = a.t0 ? a.t0[gi] : a.t0_scalar;
     T_i = a.t_hor > 0 ? a.t_hor : (a.sys.t_max - t0);
-    acc.init(T_i + 1);
+    acc.init(T_i + 1, acc_s);
     if (a.X) {
 #pragma unroll
       for (int c = 0; c < n; ++c) a.X[gi * (int64_t)(a.t_stride + 1) * n + c] = x[c];
@@ -154,8 +156,10 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       for (int c = 0; c < KIN; ++c) v[c] = 0.f;
       if (owner) {
 #pragma unroll
-        for (int c = 0; c < n; ++c) v[c] = (x[c] - nc.in_center[c]) / nc.in_half[c];
-        v[n] = ((float)t_abs - nc.in_center[n]) / nc.in_half[n];
+        // fp32 path: multiply by the reciprocal half-width (<= 1.5 ulp from the
+        // division, no FCHK / slow-path branch per input per step)
+        for (int c = 0; c < n; ++c) v[c] = (x[c] - nc.in_center[c]) * nc.in_inv_half[c];
+        v[n] = ((float)t_abs - nc.in_center[n]) * nc.in_inv_half[n];
       }
       float hv[KIN / 2], lv[KIN / 2];
 #pragma unroll
@@ -314,9 +318,10 @@ static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   constexpr int SPLIT = NT == 4 ? 1 : (NT == 2 ? (HP >= 32 ? 2 : 1) : (HP >= 64 ? 4 : HP / 16));
   auto kern = a.act == CACTO_ACT_ELU ? rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_ELU>
                                      : rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_TANH>;
-  const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + 1024;
-  if (!ensure_smem((const void*)kern, 3 * PL::SLOT + 1024))
-    return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", 3 * PL::SLOT + 1024);
+  constexpr uint32_t ACC = (uint32_t)(NT * SPLIT * 128 + 32) * 9 * 4;  // pairwise partial sums
+  const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + ACC + 1024;
+  if (!ensure_smem((const void*)kern, 3 * PL::SLOT + ACC + 1024))
+    return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", 3 * PL::SLOT + ACC + 1024);
   const int64_t per = (int64_t)NT * rtc::TILE;
   const int64_t blocks = (a.N + per - 1) / per;
   kern<<<(unsigned)blocks, NT * SPLIT * 128 + 32, bytes, st>>>(a);
