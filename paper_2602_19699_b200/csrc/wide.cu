@@ -108,51 +108,106 @@ __global__ void input_kernel(float* X, int64_t B, int ip, int in, RowSrc src, Ne
   }
 }
 
+// ---- [B][H] elementwise passes, 4 columns per thread (H % 4 == 0, 16-byte rows) ----
+CACTO_D int col_of4(int64_t e4, int H4) {  // first column of float4 e4 (32-bit modulo when it fits)
+  return 4 * (int)(e4 < 0x7fffffff ? (uint32_t)e4 % (uint32_t)H4 : e4 % H4);
+}
+#define CACTO_FOR4(e4, n4) \
+  for (int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < (n4); e4 += (int64_t)gridDim.x * blockDim.x)
+
 __global__ void bias_act_kernel(float* Z, const float* __restrict__ bias, float* A, int act, int64_t B, int H) {
-  const int64_t total = B * H;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const float z = Z[e] + bias[e % H];
-    Z[e] = z;
-    A[e] = act_value(act, z);
+  float4* Z4 = reinterpret_cast<float4*>(Z);
+  float4* A4 = reinterpret_cast<float4*>(A);
+  CACTO_FOR4(e, B * (H / 4)) {
+    const int c = col_of4(e, H / 4);
+    float4 z = Z4[e];
+    z.x += bias[c];
+    z.y += bias[c + 1];
+    z.z += bias[c + 2];
+    z.w += bias[c + 3];
+    Z4[e] = z;
+    A4[e] = make_float4(act_value(act, z.x), act_value(act, z.y), act_value(act, z.z), act_value(act, z.w));
   }
 }
 
 // G = act'(Z) * (S or broadcast row w)
 __global__ void d1_mul_kernel(float* G, const float* __restrict__ Z, const float* S, const float* w, int act,
                               int64_t B, int H) {
-  const int64_t total = B * H;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
-    G[e] = act_d1(act, Z[e]) * (S ? S[e] : w[e % H]);
+  const float4* Z4 = reinterpret_cast<const float4*>(Z);
+  CACTO_FOR4(e, B * (H / 4)) {
+    float4 s;
+    if (S) {
+      s = reinterpret_cast<const float4*>(S)[e];
+    } else {
+      const int c = col_of4(e, H / 4);
+      s = make_float4(w[c], w[c + 1], w[c + 2], w[c + 3]);
+    }
+    const float4 z = Z4[e];
+    reinterpret_cast<float4*>(G)[e] =
+        make_float4(act_d1(act, z.x) * s.x, act_d1(act, z.y) * s.y, act_d1(act, z.z) * s.z, act_d1(act, z.w) * s.w);
+  }
 }
 
 // zeta = act''(z) s rbar = h(z) g rbar  -> G ;  u_{i+1} = act'(z) rbar -> R   (nets.py:282-283)
 __global__ void zeta_u_kernel(const float* __restrict__ Z, float* G, float* R, int act, int64_t n) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const float z = Z[e], r = R[e];
-    G[e] = act_h(act, z) * G[e] * r;
-    R[e] = act_d1(act, z) * r;
+  float4* G4 = reinterpret_cast<float4*>(G);
+  float4* R4 = reinterpret_cast<float4*>(R);
+  CACTO_FOR4(e, n / 4) {
+    const float4 z = reinterpret_cast<const float4*>(Z)[e], r = R4[e], g = G4[e];
+    G4[e] = make_float4(act_h(act, z.x) * g.x * r.x, act_h(act, z.y) * g.y * r.y, act_h(act, z.z) * g.z * r.z,
+                        act_h(act, z.w) * g.w * r.w);
+    R4[e] = make_float4(act_d1(act, z.x) * r.x, act_d1(act, z.y) * r.y, act_d1(act, z.z) * r.z,
+                        act_d1(act, z.w) * r.w);
   }
 }
 
 // zbar = act'(z) abar (+ zeta)   (nets.py:225-227)
 __global__ void zbar_kernel(const float* __restrict__ Z, const float* __restrict__ ABAR, float* G, int has_zeta,
                             int act, int64_t n) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const float v = act_d1(act, Z[e]) * ABAR[e];
-    G[e] = has_zeta ? v + G[e] : v;
+  float4* G4 = reinterpret_cast<float4*>(G);
+  CACTO_FOR4(e, n / 4) {
+    const float4 z = reinterpret_cast<const float4*>(Z)[e], ab = reinterpret_cast<const float4*>(ABAR)[e];
+    float4 v = make_float4(act_d1(act, z.x) * ab.x, act_d1(act, z.y) * ab.y, act_d1(act, z.z) * ab.z,
+                           act_d1(act, z.w) * ab.w);
+    if (has_zeta) {
+      const float4 g = G4[e];
+      v = make_float4(v.x + g.x, v.y + g.y, v.z + g.z, v.w + g.w);
+    }
+    G4[e] = v;
   }
 }
 
-// OUT[b][h] = sum_j DEL[b][j] * W[j][h]   (small K = out: abar = delta W_L)
-__global__ void outer_kernel(float* OUT, const float* __restrict__ DEL, int ldd, int nout, const float* __restrict__ W,
-                             int H, int64_t B) {
-  const int64_t total = B * H;
+// top hidden layer of the value-path backprop: abar = delta W_L (small K = out)
+// and zbar = act'(z) abar (+ zeta) in one pass, 4 columns per thread
+// (nets.py:221-227; replaces an outer-product pass + zbar_kernel)
+__global__ void outer_zbar_kernel(float* G, const float* __restrict__ Z, const float* __restrict__ DEL, int ldd,
+                                  int nout, const float* __restrict__ W, int has_zeta, int act, int H, int64_t B) {
+  const int H4 = H >> 2;
+  const int64_t total = B * H4;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = e / H;
-    const int h = (int)(e - b * H);
-    float s = 0.f;
-    for (int j = 0; j < nout; ++j) s = fmaf(DEL[b * ldd + j], W[(int64_t)j * H + h], s);
-    OUT[e] = s;
+    const int64_t b = e / H4;
+    const int h = (int)(e - b * H4) * 4;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < nout; ++j) {
+      const float d = DEL[b * ldd + j];
+      const float4 w = *reinterpret_cast<const float4*>(W + (int64_t)j * H + h);
+      s[0] = fmaf(d, w.x, s[0]);
+      s[1] = fmaf(d, w.y, s[1]);
+      s[2] = fmaf(d, w.z, s[2]);
+      s[3] = fmaf(d, w.w, s[3]);
+    }
+    const int64_t o = b * H + h;
+    const float4 z = *reinterpret_cast<const float4*>(Z + o);
+    float4 r = make_float4(act_d1(act, z.x) * s[0], act_d1(act, z.y) * s[1], act_d1(act, z.z) * s[2],
+                           act_d1(act, z.w) * s[3]);
+    if (has_zeta) {
+      const float4 g = *reinterpret_cast<const float4*>(G + o);
+      r.x += g.x;
+      r.y += g.y;
+      r.z += g.z;
+      r.w += g.w;
+    }
+    *reinterpret_cast<float4*>(G + o) = r;
   }
 }
 
@@ -392,7 +447,7 @@ static int forward(const Ctx& c, const WNet& w, const Acts& a, int64_t B) {
     float* A = a.A + (size_t)i * B * H;
     int rc = gemm(c, (int)B, H, w.cols(i), cur, width, 1, w.W(i), w.cols(i), 1, Z, H, 0);
     if (rc) return rc;
-    bias_act_kernel<<<grid1d(B * H), 256, 0, c.st>>>(Z, w.b(i), A, w.sh.act, B, H);
+    bias_act_kernel<<<grid1d(B * H / 4), 256, 0, c.st>>>(Z, w.b(i), A, w.sh.act, B, H);
     cur = A;
     width = H;
   }
@@ -403,12 +458,12 @@ static int forward(const Ctx& c, const WNet& w, const Acts& a, int64_t B) {
 static int sweep(const Ctx& c, const WNet& w, const Acts& a, int64_t B, int j, float* S, float* S0) {
   const int nh = w.sh.nh, H = w.H;
   const int64_t TS = B * H;
-  d1_mul_kernel<<<grid1d(TS), 256, 0, c.st>>>(a.G + (nh - 1) * TS, a.Z + (nh - 1) * TS, nullptr,
+  d1_mul_kernel<<<grid1d(TS / 4), 256, 0, c.st>>>(a.G + (nh - 1) * TS, a.Z + (nh - 1) * TS, nullptr,
                                               w.W(nh) + (int64_t)j * H, w.sh.act, B, H);
   for (int i = nh - 1; i >= 1; --i) {
     int rc = gemm(c, (int)B, H, H, a.G + i * TS, H, 1, w.W(i), 1, H, S, H, 0);
     if (rc) return rc;
-    d1_mul_kernel<<<grid1d(TS), 256, 0, c.st>>>(a.G + (i - 1) * TS, a.Z + (i - 1) * TS, S, nullptr, w.sh.act, B, H);
+    d1_mul_kernel<<<grid1d(TS / 4), 256, 0, c.st>>>(a.G + (i - 1) * TS, a.Z + (i - 1) * TS, S, nullptr, w.sh.act, B, H);
   }
   return gemm(c, (int)B, w.ip, H, a.G, H, 1, w.W(0), 1, w.ip, S0, w.ip, 0);
 }
@@ -427,10 +482,13 @@ static int backprop(const Ctx& c, const WNet& w, const Acts& a, int64_t B, const
   rc = colsum(c, DEL, ldd, nullptr, 0, B, out, grad + w.lo.b[nh]);
   if (rc) return rc;
   if (nh == 0) return CACTO_OK;
-  outer_kernel<<<grid1d(TS), 256, 0, c.st>>>(ABAR, DEL, ldd, out, w.W(nh), H, B);
   for (int i = nh - 1; i >= 0; --i) {
     float* G = a.G + i * TS;
-    zbar_kernel<<<grid1d(TS), 256, 0, c.st>>>(a.Z + i * TS, ABAR, G, has_zeta ? 1 : 0, w.sh.act, TS);
+    if (i == nh - 1)
+      outer_zbar_kernel<<<grid1d(TS / 4), 256, 0, c.st>>>(G, a.Z + i * TS, DEL, ldd, out, w.W(nh), has_zeta ? 1 : 0,
+                                                          w.sh.act, H, B);
+    else
+      zbar_kernel<<<grid1d(TS / 4), 256, 0, c.st>>>(a.Z + i * TS, ABAR, G, has_zeta ? 1 : 0, w.sh.act, TS);
     rc = colsum(c, G, H, nullptr, 0, B, H, grad + w.lo.b[i]);
     if (rc) return rc;
     const float* ai = i == 0 ? a.X0 : a.A + (i - 1) * TS;
@@ -628,7 +686,7 @@ int wide_critic_loss(const cacto_mlp_t* cm, const cacto_mlp_t* tm, const cacto_b
     if (rc) return rc;
     rc = gemm(c, H, w.cols(i), (int)B, a.G + i * TS, 1, H, U, 1, uw, slot + w.lo.w[i], w.cols(i), 1);  // g^T u
     if (rc) return rc;
-    zeta_u_kernel<<<grid1d(TS), 256, 0, st>>>(a.Z + i * TS, a.G + i * TS, Rcur, w.sh.act, TS);
+    zeta_u_kernel<<<grid1d(TS / 4), 256, 0, st>>>(a.Z + i * TS, a.G + i * TS, Rcur, w.sh.act, TS);
     U = Rcur;
     uw = H;
     float* t = Rcur;
