@@ -28,6 +28,8 @@
 // Split-K (tile index carries the split) writes per-split partials (deterministic reduce after).
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "tc.cuh"
 
 namespace cacto {
@@ -386,13 +388,25 @@ __global__ void splitk_reduce_warp_kernel(const float* __restrict__ part, int sp
 // (256 only for N >= 512: at N = 256 the halved tile count quantises badly on 148 SMs)
 static int tile_bn(int N) { return N <= 64 ? 64 : (N >= 512 && N % 256 == 0 ? 256 : 128); }
 
+// split-K when the tile grid cannot fill the GPU and K is long (weight gradients):
+// as many splits as fill the SMs (not only powers of two), >= 8 k-blocks each,
+// never an empty split
+static int choose_splits(int tiles, int nkb) {
+  if (tiles * 2 > num_sms()) return 1;
+  int splits = std::max(1, std::min(num_sms() / tiles, nkb / 8));
+  if (splits > 1) {
+    const int per = (nkb + splits - 1) / splits;
+    splits = (nkb + per - 1) / per;
+  }
+  return splits;
+}
+
 // workspace bytes a gemm of this shape may need for split-K partials
 size_t gemm_workspace_bytes(int M, int N, int K) {
   const int bn = tile_bn(N);
   const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + bn - 1) / bn);
   const int nkb = (K + tc::BK - 1) / tc::BK;
-  int splits = 1;
-  while (tiles * splits * 2 <= num_sms() && nkb / (splits * 2) >= 8) splits *= 2;
+  const int splits = choose_splits(tiles, nkb);
   return splits > 1 ? (size_t)splits * M * N * 4 : 0;
 }
 
@@ -414,8 +428,7 @@ int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, con
   // split-K when the tile grid cannot fill the GPU and K is long (weight gradients)
   const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + bn - 1) / bn);
   const int nkb = (K + tc::BK - 1) / tc::BK;
-  int splits = 1;
-  while (tiles * splits * 2 <= num_sms() && nkb / (splits * 2) >= 8) splits *= 2;
+  int splits = choose_splits(tiles, nkb);
   if (splits > 1 && (!ws || ws_bytes < (size_t)splits * M * N * 4)) splits = 1;
   g.kb_per_split = (nkb + splits - 1) / splits;
   if (g.kb_per_split > 0) splits = (nkb + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
