@@ -386,7 +386,10 @@ __global__ void splitk_reduce_warp_kernel(const float* __restrict__ part, int sp
 
 // output tile width for an N-column GEMM
 // (256 only for N >= 512: at N = 256 the halved tile count quantises badly on 148 SMs)
-static int tile_bn(int N) { return N <= 64 ? 64 : (N >= 512 && N % 256 == 0 ? 256 : 128); }
+// (96 for 65..96 columns, e.g. the critic's 65-column [W|b] reductions: 25 % fewer MMA columns than 128)
+static int tile_bn(int N) {
+  return N <= 64 ? 64 : (N <= 96 ? 96 : (N >= 512 && N % 256 == 0 ? 256 : 128));
+}
 
 // split-K when the tile grid cannot fill the GPU and K is long (weight gradients):
 // as many splits as fill the SMs (not only powers of two), >= 8 k-blocks each,
@@ -445,6 +448,7 @@ int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, con
     g.split_stride = 0;
   }
   rc = bn == 64    ? tc::launch_gemm<64>(ma, mb, g, splits, st)
+       : bn == 96  ? tc::launch_gemm<96>(ma, mb, g, splits, st)
        : bn == 128 ? tc::launch_gemm<128>(ma, mb, g, splits, st)
                    : tc::launch_gemm<256>(ma, mb, g, splits, st);
   if (rc || splits == 1) return rc;

@@ -37,7 +37,10 @@ def run(M, N, K, a_kmajor, b_kmajor, passes, accumulate=False, alpha=1.0, seed=0
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 128, 64), (300, 200, 100), (64, 64, 512),
                                    (1000, 512, 512), (128, 8, 64), (5, 300, 36), (512, 512, 20000),
-                                   (300, 96, 4000)])
+                                   (300, 96, 4000),
+                                   # 96-wide tiles (65..96 columns), incl. the critic's K = 2B reduction
+                                   # shape with split-K over every SM; 256-wide tiles (N >= 512)
+                                   (64, 68, 131072), (200, 72, 3000), (130, 768, 96)])
 @pytest.mark.parametrize("a_k,b_k", [(True, True), (False, True), (True, False), (False, False)])
 def test_gemm_3xtf32(M, N, K, a_k, b_k):
     if (not a_k and M % 4) or (not b_k and N % 4):
