@@ -38,6 +38,7 @@ struct RolloutArgs {
   NetConst<T> pre_nc[2];
   int score_mode;        // CACTO_SCORE_*
   T* scores;
+  int cta_rows;          // tensor-core rollout: starts per CTA (set by its launcher)
 };
 
 // NumPy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) for

@@ -28,6 +28,8 @@
 #include <cuda_fp16.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "net.cuh"
 #include "rollout.cuh"
 #include "systems.cuh"
@@ -90,8 +92,14 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   const int q = warp & 3;
   const int part = (warp % WPT) >> 2;
   const int r = (q << 5) + lane;
-  const int64_t gi = ((int64_t)blockIdx.x * NT + g) * TILE + r;
-  const bool owner = epi && part == 0 && gi < a.N;
+  // the CTA's starts: cta_rows (a multiple of 32, <= NT * TILE) so that the grid
+  // covers every SM; warps whose 32 rows are all past the CTA's range keep the
+  // barrier protocol but skip the math (their TMEM lanes carry no start)
+  const int64_t cta0 = (int64_t)blockIdx.x * a.cta_rows;
+  const int lrow = g * TILE + r;
+  const int64_t gi = cta0 + lrow;
+  const bool live = (g * TILE + q * 32) < a.cta_rows && cta0 + g * TILE + q * 32 < a.N;
+  const bool owner = epi && part == 0 && lrow < a.cta_rows && gi < a.N;
   float x[n];
   int t0 = 0, T_i = 0;
   PairwiseSumS<float> acc;
@@ -189,8 +197,10 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     };
     auto start_pass = [&](int P) {
       const int slot = P < n_pre ? P + 1 : 0;
-      write_input(slot, P < n_pre ? t0 : t0 + (P - n_pre));
-      preload_bias(slot, 0);
+      if (live) {
+        write_input(slot, P < n_pre ? t0 : t0 + (P - n_pre));
+        preload_bias(slot, 0);
+      }
       handoff();
     };
     if (npass > 0) start_pass(0);
@@ -198,6 +208,10 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       const int slot = P < n_pre ? P + 1 : 0;
       for (int l = 0; l < nh; ++l) {  // hidden layers
         wait_done();
+        if (!live) {
+          handoff();
+          continue;
+        }
         // 16-column chunks, software pipelined: the next chunk's tcgen05.ld is in
         // flight while this chunk's activations are computed and stored (a single
         // warp's ld + wait costs ~160 cycles, profiles/probe_tmem.cu)
@@ -231,7 +245,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       // output layer
       wait_done();
       float o[16];
-      if (part == 0) tc::tmem_ld16_wait(t_d, o);
+      if (part == 0 && live) tc::tmem_ld16_wait(t_d, o);
       if (slot != 0) {
         // scoring net: sigma(x0) = sigma_min + softplus(o) or V(x0) = o
         const float ov = o[0] * (1.f / WSCALE);
@@ -322,9 +336,16 @@ static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + ACC + 1024;
   if (!ensure_smem((const void*)kern, 3 * PL::SLOT + ACC + 1024))
     return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", 3 * PL::SLOT + ACC + 1024);
-  const int64_t per = (int64_t)NT * rtc::TILE;
-  const int64_t blocks = (a.N + per - 1) / per;
-  kern<<<(unsigned)blocks, NT * SPLIT * 128 + 32, bytes, st>>>(a);
+  // starts per CTA: as even as 32-row granularity allows over whole waves of SMs
+  // (65,536 starts: 147 CTAs of 448 instead of 128 CTAs of 512 leaving 20 SMs idle)
+  const int64_t per = (int64_t)NT * rtc::TILE, sms = num_sms();
+  const int64_t waves = std::max<int64_t>(1, (a.N + per * sms - 1) / (per * sms));
+  int64_t rows = (a.N + waves * sms - 1) / (waves * sms);
+  rows = std::min<int64_t>(per, (rows + 31) / 32 * 32);
+  RolloutArgs<float> b = a;
+  b.cta_rows = (int)rows;
+  const int64_t blocks = (a.N + rows - 1) / rows;
+  kern<<<(unsigned)blocks, NT * SPLIT * 128 + 32, bytes, st>>>(b);
   return check_launch("rollout_tc_kernel");
 }
 
