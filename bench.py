@@ -406,7 +406,7 @@ def main():
         kname = "rollout_kernel (K1 SIMT, cost-only over all candidates)"
     traffic = None
     prof = ROOT / "profiles" / "rollout_ncu_summary.json"
-    if prof.exists():
+    if prof.exists() and args.workload == "dubins" and args.precision == "fp32":  # the captured launch
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:

@@ -93,12 +93,12 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   const int part = (warp % WPT) >> 2;
   const int r = (q << 5) + lane;
   // the CTA's starts: cta_rows (a multiple of 32, <= NT * TILE) so that the grid
-  // covers every SM; warps whose 32 rows are all past the CTA's range keep the
-  // barrier protocol but skip the math (their TMEM lanes carry no start)
+  // covers every SM; lanes past the CTA's range run the same code on zero inputs
+  // and write nothing (skipping the math in whole idle warps measured slower: the
+  // extra branch cost registers -> spills)
   const int64_t cta0 = (int64_t)blockIdx.x * a.cta_rows;
   const int lrow = g * TILE + r;
   const int64_t gi = cta0 + lrow;
-  const bool live = (g * TILE + q * 32) < a.cta_rows && cta0 + g * TILE + q * 32 < a.N;
   const bool owner = epi && part == 0 && lrow < a.cta_rows && gi < a.N;
   float x[n];
   int t0 = 0, T_i = 0;
@@ -197,10 +197,8 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     };
     auto start_pass = [&](int P) {
       const int slot = P < n_pre ? P + 1 : 0;
-      if (live) {
-        write_input(slot, P < n_pre ? t0 : t0 + (P - n_pre));
-        preload_bias(slot, 0);
-      }
+      write_input(slot, P < n_pre ? t0 : t0 + (P - n_pre));
+      preload_bias(slot, 0);
       handoff();
     };
     if (npass > 0) start_pass(0);
@@ -208,10 +206,6 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       const int slot = P < n_pre ? P + 1 : 0;
       for (int l = 0; l < nh; ++l) {  // hidden layers
         wait_done();
-        if (!live) {
-          handoff();
-          continue;
-        }
         // 16-column chunks, software pipelined: the next chunk's tcgen05.ld is in
         // flight while this chunk's activations are computed and stored (a single
         // warp's ld + wait costs ~160 cycles, profiles/probe_tmem.cu)
@@ -245,7 +239,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       // output layer
       wait_done();
       float o[16];
-      if (part == 0 && live) tc::tmem_ld16_wait(t_d, o);
+      if (part == 0) tc::tmem_ld16_wait(t_d, o);
       if (slot != 0) {
         // scoring net: sigma(x0) = sigma_min + softplus(o) or V(x0) = o
         const float ov = o[0] * (1.f / WSCALE);
