@@ -18,39 +18,56 @@ struct Cols {
   int width[5];
 };
 
+// One warp per group of 32 sampled rows: the warp loads the 32 indices once
+// (one coalesced 256 B read), then copies each column's contiguous
+// [32 x width] output block with consecutive lanes on consecutive elements; the
+// source row of element e is broadcast from lane e / width by a shuffle, so all
+// index arithmetic is 32-bit and there is no per-element 64-bit division.
 template <typename T>
-__global__ void gather_kernel(Cols<T> c, const int64_t* __restrict__ idx, const int64_t* cycle, int64_t stride,
-                              int64_t B) {
+__global__ void __launch_bounds__(256) gather_kernel(Cols<T> c, const int64_t* __restrict__ idx,
+                                                     const int64_t* cycle, int64_t stride, int64_t B) {
   if (cycle) idx += (*cycle) * stride;
-  const int W = c.width[0] + c.width[1] + c.width[2] + c.width[3] + c.width[4];
-  const int64_t total = B * W;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t b = e / W;
-    int f = (int)(e - b * W);
-    int col = 0;
-    while (f >= c.width[col]) {
-      f -= c.width[col];
-      ++col;
+  const int lane = threadIdx.x & 31;
+  const int64_t groups = (B + 31) >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < groups; g += nwarps) {
+    const int64_t b0 = g << 5;
+    const int nb = B - b0 < 32 ? (int)(B - b0) : 32;
+    const int64_t my_row = lane < nb ? __ldg(idx + b0 + lane) : 0;
+#pragma unroll
+    for (int col = 0; col < 5; ++col) {
+      const int w = c.width[col];
+      const int tot = nb * w;
+      const int span = ((32 * w) + 31) & ~31;  // uniform trip count: every lane joins the shuffles
+      const T* __restrict__ src = c.src[col];
+      T* __restrict__ dst = c.dst[col] + b0 * w;
+      for (int e = lane; e < span; e += 32) {
+        const int r = e / w;
+        const int64_t row = __shfl_sync(0xffffffffu, my_row, r & 31);
+        if (e < tot) dst[e] = __ldg(src + row * w + (e - r * w));
+      }
     }
-    int64_t row = __ldg(idx + b);
-    c.dst[col][b * c.width[col] + f] = __ldg(c.src[col] + row * c.width[col] + f);
   }
 }
 
+// FIFO append: row r lands in slot (cursor + r) % capacity, so within one column
+// element e of the source goes to (cursor * w + e) mod (capacity * w) -- both
+// sides contiguous, the modulo a single conditional subtract (cursor < capacity,
+// rows <= capacity).
 template <typename T>
 __global__ void ring_push_kernel(Cols<T> c, int64_t rows, int64_t capacity, int64_t cursor) {
-  const int W = c.width[0] + c.width[1] + c.width[2] + c.width[3] + c.width[4];
-  const int64_t total = rows * W;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = e / W;
-    int f = (int)(e - r * W);
-    int col = 0;
-    while (f >= c.width[col]) {
-      f -= c.width[col];
-      ++col;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+#pragma unroll
+  for (int col = 0; col < 5; ++col) {
+    const int64_t w = c.width[col];
+    const int64_t total = rows * w, cap_w = capacity * w, base = cursor * w;
+    const T* __restrict__ src = c.src[col];
+    T* __restrict__ dst = c.dst[col];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += step) {
+      int64_t o = base + e;
+      if (o >= cap_w) o -= cap_w;
+      dst[o] = src[e];
     }
-    int64_t slot = (cursor + r) % capacity;
-    c.dst[col][slot * c.width[col] + f] = c.src[col][r * c.width[col] + f];
   }
 }
 
@@ -140,18 +157,17 @@ extern "C" int cacto_gather(const cacto_batch_t* ring, void* xa, void* u, void* 
   if (ring->rows < 0) return set_error(CACTO_EVALUE, "gather: negative rows");
   if (ring->rows == 0) return CACTO_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  int64_t W = 3 * ring->n + ring->m + 3;
   if (ring->dtype == CACTO_F32) {
     Cols<float> c = batch_cols<float>(ring);
     c.dst[0] = (float*)xa; c.dst[1] = (float*)u; c.dst[2] = (float*)v_bar; c.dst[3] = (float*)v_bar_x;
     c.dst[4] = (float*)xa_plus_k;
-    gather_kernel<float><<<grid_for(ring->rows * W), 256, 0, st>>>(c, ring->idx, ring->cycle, ring->idx_stride,
+    gather_kernel<float><<<grid_for(ring->rows * 8), 256, 0, st>>>(c, ring->idx, ring->cycle, ring->idx_stride,
                                                                     ring->rows);
   } else {
     Cols<double> c = batch_cols<double>(ring);
     c.dst[0] = (double*)xa; c.dst[1] = (double*)u; c.dst[2] = (double*)v_bar; c.dst[3] = (double*)v_bar_x;
     c.dst[4] = (double*)xa_plus_k;
-    gather_kernel<double><<<grid_for(ring->rows * W), 256, 0, st>>>(c, ring->idx, ring->cycle, ring->idx_stride,
+    gather_kernel<double><<<grid_for(ring->rows * 8), 256, 0, st>>>(c, ring->idx, ring->cycle, ring->idx_stride,
                                                                      ring->rows);
   }
   return check_launch("gather_kernel");
@@ -160,7 +176,7 @@ extern "C" int cacto_gather(const cacto_batch_t* ring, void* xa, void* u, void* 
 extern "C" int cacto_ring_push(const cacto_batch_t* src, void* ring_xa, void* ring_u, void* ring_v_bar,
                                void* ring_v_bar_x, void* ring_xa_plus_k, int64_t capacity, int64_t cursor,
                                void* stream) {
-  if (!src || capacity < 1 || src->rows > capacity || src->rows < 0)
+  if (!src || capacity < 1 || src->rows > capacity || src->rows < 0 || cursor < 0 || cursor >= capacity)
     return set_error(CACTO_EVALUE, "ring_push: bad sizes");
   if (src->rows == 0) return CACTO_OK;
   cudaStream_t st = (cudaStream_t)stream;

@@ -106,19 +106,29 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
       if (c) atomicAdd(&st->hist[p][d], c);
     }
     grid.sync();
-    if (tid == 0) {
-      long long cum = 0;
-      int digit = 255;
-      for (int d = 0; d < 256; ++d) {
-        long long h = st->hist[p][d];
-        if (cum + h >= need) {
-          digit = d;
-          break;
-        }
-        cum += h;
+    {
+      // threshold digit: block-wide inclusive scan of the 256 bins (one bin per
+      // thread), the first digit whose running count reaches `need`
+      static_assert(kSelThreads == 256, "one histogram bin per thread");
+      const unsigned int h = __ldcg(&st->hist[p][tid]);
+      unsigned int x = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
       }
-      s_need = need - cum;
-      s_prefix = prefix | ((unsigned long long)digit << shift);
+      if (lane == 31) s_warp[warp] = x;
+      __syncthreads();
+      long long incl = x;
+      for (int w = 0; w < warp; ++w) incl += s_warp[w];
+      const long long excl = incl - h;
+      if (incl >= need && excl < need) {
+        s_need = need - excl;
+        s_prefix = prefix | ((unsigned long long)tid << shift);
+      } else if (tid == 255 && incl < need) {  // unreachable for consistent counts
+        s_need = need - incl;
+        s_prefix = prefix | (255ull << shift);
+      }
     }
     __syncthreads();
     prefix = s_prefix;
@@ -146,12 +156,16 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
   }
   grid.sync();
   __shared__ long long s_off;
-  if (tid == 0) {
+  {
     long long off = 0;
-    for (int b = 0; b < blockIdx.x; ++b) off += st->block_eq[b];
-    s_off = off;
+    for (int b = tid; b < (int)blockIdx.x; b += kSelThreads) off += __ldcg(&st->block_eq[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+    if (tid == 0) s_off = 0;
+    __syncthreads();
+    if (lane == 0 && off) atomicAdd((unsigned long long*)&s_off, (unsigned long long)off);
+    __syncthreads();
   }
-  __syncthreads();
   long long running = s_off;
   for (int64_t base = c0; base < c1; base += kSelThreads) {
     int64_t i = base + tid;
@@ -178,31 +192,59 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
   }
 }
 
-// bitonic sort of kSortChunk-pair chunks (pads with +inf pairs): one thread per
-// compare-exchange pair (kSortChunk / 2 threads), no idle lanes in any round
+// bitonic sort of kSortChunk-pair chunks (pads with +inf pairs), register
+// resident: warp w owns positions [64w, 64w + 64), lane l holds 64w + l and
+// 64w + 32 + l.  Exchanges at distance j = 32 stay inside a thread, j < 32 are
+// warp shuffles; only the 15 rounds with j >= 64 go through shared memory
+// (two barriers each) -- 30 barriers instead of one per round (66).
 constexpr int kSortThreads = kSortChunk / 2;
+
+CACTO_D Pair shfl_pair(const Pair& v, int j) {
+  return Pair{__shfl_xor_sync(0xffffffffu, v.key, j), __shfl_xor_sync(0xffffffffu, v.idx, j)};
+}
+// element at position i keeps min(a, b) if it is the lower of the pair in an
+// ascending run, or the upper one in a descending run
+CACTO_D Pair bitonic_keep(const Pair& a, const Pair& b, int i, int j, int k) {
+  const bool take_min = ((i & k) == 0) == ((i & j) == 0);
+  return (pair_less(b, a) == take_min) ? b : a;
+}
+
 __global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(Pair* data, int64_t M) {
   __shared__ Pair sh[kSortChunk];
   const int64_t base = (int64_t)blockIdx.x * kSortChunk;
-  for (int i = threadIdx.x; i < kSortChunk; i += kSortThreads)
-    sh[i] = (base + i < M) ? data[base + i] : Pair{~0ull, 0x7fffffffffffffffll};
-  __syncthreads();
-  const int p = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p0 = warp * 64 + lane, p1 = p0 + 32;
+  const Pair pad{~0ull, 0x7fffffffffffffffll};
+  Pair v0 = (base + p0 < M) ? data[base + p0] : pad;
+  Pair v1 = (base + p1 < M) ? data[base + p1] : pad;
   for (int k = 2; k <= kSortChunk; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));  // insert a 0 bit at log2(j)
-      const int ixj = i | j;
-      const bool up = (i & k) == 0;
-      const Pair a = sh[i], b = sh[ixj];
-      if (pair_less(b, a) == up) {
-        sh[i] = b;
-        sh[ixj] = a;
-      }
+    int j = k >> 1;
+    for (; j >= 64; j >>= 1) {
+      sh[p0] = v0;
+      sh[p1] = v1;
       __syncthreads();
+      const Pair b0 = sh[p0 ^ j], b1 = sh[p1 ^ j];
+      __syncthreads();
+      v0 = bitonic_keep(v0, b0, p0, j, k);
+      v1 = bitonic_keep(v1, b1, p1, j, k);
+    }
+    if (j == 32) {
+      const bool up = (p0 & k) == 0;
+      if (pair_less(v1, v0) == up) {
+        const Pair t = v0;
+        v0 = v1;
+        v1 = t;
+      }
+      j = 16;
+    }
+    for (; j > 0; j >>= 1) {
+      const Pair b0 = shfl_pair(v0, j), b1 = shfl_pair(v1, j);
+      v0 = bitonic_keep(v0, b0, p0, j, k);
+      v1 = bitonic_keep(v1, b1, p1, j, k);
     }
   }
-  for (int i = threadIdx.x; i < kSortChunk; i += kSortThreads)
-    if (base + i < M) data[base + i] = sh[i];
+  if (base + p0 < M) data[base + p0] = v0;
+  if (base + p1 < M) data[base + p1] = v1;
 }
 
 // merge adjacent sorted runs of width w into runs of width 2w

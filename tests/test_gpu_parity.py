@@ -552,3 +552,38 @@ def test_update_engine_matches_oracle_loop(graphs, fp64):
     # a second run continues the streams (Adam steps, buffer) like the reference's next iteration
     closs2, _ = eng.run(M, np.random.default_rng(10))
     assert np.all(np.isfinite(closs2))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("n,m,cap,pushes,bsz", [(4, 2, 777, (500, 700, 3), 1000), (15, 6, 64, (64, 1), 33),
+                                                (6, 3, 4096, (4096, 2049), 4097)])
+def test_ring_push_wrap_and_gather_bitwise(prec, n, m, cap, pushes, bsz):
+    """FIFO push with wrap-around (buffer.py:108-130) and the warp-per-32-rows gather
+    (buffer.py:132-138) vs the same ring restated in NumPy, ragged batch sizes."""
+    from paper_2602_19699_b200.device import set_precision, get_precision
+    old = get_precision()
+    set_precision(prec)
+    try:
+        rng = np.random.default_rng(cap + bsz)
+        buf = B_buffer.ReplayBuffer(n, m, 60, capacity=cap)
+        widths = (n + 1, m, None, n, n + 1)
+        ring = [np.zeros((cap,) + ((w,) if w else ())) for w in widths]
+        cursor = size = 0
+        for cnt in pushes:
+            cols = [rng.standard_normal((cnt,) + ((w,) if w else ())) for w in widths]
+            buf.push_many(B_buffer.SampleBatch(*cols, 60))
+            first = max(0, cnt - cap)
+            for r in range(first, cnt):
+                for c, col in zip(ring, cols):
+                    c[(cursor + r - first) % cap] = col[r]
+            cursor = (cursor + cnt - first) % cap
+            size = min(size + cnt - first, cap)
+        assert len(buf) == size
+        dt = torch.float32 if prec == "fp32" else torch.float64
+        idx = rng.integers(0, size, size=bsz)
+        got = buf.gather_device(torch.as_tensor(idx, device="cuda"))
+        for g, c in zip(got, ring):
+            want = torch.as_tensor(c[idx]).to(dt).numpy()
+            np.testing.assert_array_equal(g.cpu().numpy().reshape(want.shape), want)
+    finally:
+        set_precision(old)
