@@ -59,6 +59,7 @@ CACTO_D double key_score(unsigned long long k, double*) {
 constexpr int kSelThreads = 256;
 constexpr int kSortChunk = 2048;
 constexpr int kMaxSelBlocks = 1024;
+constexpr int kSelBatch = 4;  // candidates per thread per histogram sweep
 
 struct SelState {
   unsigned int hist[8][256];
@@ -87,15 +88,26 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
     const int shift = KB - 8 * (p + 1);
     for (int q = tid; q < (kSelThreads / 32) * 256; q += kSelThreads) (&wh[0][0])[q] = 0;
     __syncthreads();
-    for (int64_t i = c0 + tid; i < c1; i += kSelThreads) {
-      unsigned long long k = score_key(scores[i]);
-      bool match = (p == 0) || ((k >> (shift + 8)) == (prefix >> (shift + 8)));
-      if (match) {
-        unsigned int d = (unsigned int)((k >> shift) & 255ull);
-        // warp-aggregated increment: lanes with the same digit combine
-        unsigned int peers = __match_any_sync(__activemask(), d);
-        int leader = __ffs(peers) - 1;
-        if (lane == leader) atomicAdd(&wh[warp][d], (unsigned int)__popc(peers));
+    // kSelBatch independent loads in flight per thread before the histogram updates
+    for (int64_t i0 = c0 + tid; i0 < c1; i0 += kSelBatch * kSelThreads) {
+      T v[kSelBatch];
+#pragma unroll
+      for (int u = 0; u < kSelBatch; ++u) {
+        const int64_t i = i0 + u * kSelThreads;
+        v[u] = i < c1 ? scores[i] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kSelBatch; ++u) {
+        const unsigned long long k = score_key(v[u]);
+        const bool match = (i0 + u * kSelThreads < c1) &&
+                           ((p == 0) || ((k >> (shift + 8)) == (prefix >> (shift + 8))));
+        if (match) {
+          unsigned int d = (unsigned int)((k >> shift) & 255ull);
+          // warp-aggregated increment: lanes with the same digit combine
+          unsigned int peers = __match_any_sync(__activemask(), d);
+          int leader = __ffs(peers) - 1;
+          if (lane == leader) atomicAdd(&wh[warp][d], (unsigned int)__popc(peers));
+        }
       }
     }
     __syncthreads();
@@ -335,7 +347,9 @@ static int select_entry(const T* scores, int64_t N, int64_t keep, int64_t base_i
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSelThreads, 0);
   if (occ < 1) occ = 1;
-  int64_t want = (N + kSelThreads * 8 - 1) / (kSelThreads * 8);
+  // one load batch per thread when the grid allows (65,536 candidates -> 64 CTAs):
+  // each pass is then one round of L2 latency, not eight
+  int64_t want = (N + kSelThreads * kSelBatch - 1) / (kSelThreads * kSelBatch);
   int64_t cap = (int64_t)occ * num_sms();
   if (cap > kMaxSelBlocks) cap = kMaxSelBlocks;
   int G = (int)(want < 1 ? 1 : (want > cap ? cap : want));
