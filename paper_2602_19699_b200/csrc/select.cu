@@ -28,6 +28,25 @@ CACTO_D bool pair_less(const Pair& a, const Pair& b) {
   return a.key < b.key || (a.key == b.key && a.idx < b.idx);
 }
 
+// fp32 scores with N < 2^32: (32-bit key, 32-bit index) packed in one 64-bit
+// word whose unsigned order is the pair order -- half the bytes per sort step
+// and a single compare.  fp64 (64-bit keys) and shard merges keep `Pair`.
+typedef unsigned long long Packed;
+CACTO_D bool elem_less(Packed a, Packed b) { return a < b; }
+CACTO_D bool elem_less(const Pair& a, const Pair& b) { return pair_less(a, b); }
+CACTO_D void make_elem(Packed& e, unsigned long long k, long long i) { e = (k << 32) | (unsigned long long)(unsigned int)i; }
+CACTO_D void make_elem(Pair& e, unsigned long long k, long long i) { e = Pair{k, i}; }
+CACTO_D void make_pad(Packed& e) { e = ~0ull; }
+CACTO_D void make_pad(Pair& e) { e = Pair{~0ull, 0x7fffffffffffffffll}; }
+CACTO_D unsigned long long elem_key(Packed e) { return e >> 32; }
+CACTO_D unsigned long long elem_key(const Pair& e) { return e.key; }
+CACTO_D long long elem_idx(Packed e) { return (long long)(e & 0xffffffffull); }
+CACTO_D long long elem_idx(const Pair& e) { return e.idx; }
+CACTO_D Packed shfl_elem(Packed v, int j) { return __shfl_xor_sync(0xffffffffu, v, j); }
+CACTO_D Pair shfl_elem(const Pair& v, int j) {
+  return Pair{__shfl_xor_sync(0xffffffffu, v.key, j), __shfl_xor_sync(0xffffffffu, v.idx, j)};
+}
+
 // keys: NaN -> (max - 1), the max key is reserved for padding rows of merged runs
 CACTO_D unsigned long long score_key(float s) {
   if (s != s) return 0xFFFFFFFEull;  // NaN last
@@ -67,9 +86,9 @@ struct SelState {
   unsigned int block_eq[kMaxSelBlocks];
 };
 
-template <typename T, int KB>
+template <typename T, int KB, typename E>
 __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __restrict__ scores, int64_t N,
-                                                                   int64_t keep, SelState* st, Pair* __restrict__ sel) {
+                                                                   int64_t keep, SelState* st, E* __restrict__ sel) {
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned int wh[kSelThreads / 32][256];
   __shared__ unsigned long long s_prefix;
@@ -186,7 +205,7 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
     bool eq = i < c1 && k == kstar;
     if (lt) {
       unsigned long long slot = atomicAdd(&st->n_lt, 1ull);
-      sel[slot] = Pair{k, (long long)i};
+      make_elem(sel[slot], k, (long long)i);
     }
     unsigned int b = __ballot_sync(0xffffffffu, eq);
     if (lane == 0) s_warp[warp] = __popc(b);
@@ -197,7 +216,7 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
     for (int w = 0; w < kSelThreads / 32; ++w) tot += s_warp[w];
     if (eq) {
       long long r = woff + __popc(b & ((1u << lane) - 1u));
-      if (r < need_eq) sel[n_lt_total + r] = Pair{k, (long long)i};
+      if (r < need_eq) make_elem(sel[n_lt_total + r], k, (long long)i);
     }
     running += tot;
     __syncthreads();
@@ -211,46 +230,46 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
 // (two barriers each) -- 30 barriers instead of one per round (66).
 constexpr int kSortThreads = kSortChunk / 2;
 
-CACTO_D Pair shfl_pair(const Pair& v, int j) {
-  return Pair{__shfl_xor_sync(0xffffffffu, v.key, j), __shfl_xor_sync(0xffffffffu, v.idx, j)};
-}
 // element at position i keeps min(a, b) if it is the lower of the pair in an
 // ascending run, or the upper one in a descending run
-CACTO_D Pair bitonic_keep(const Pair& a, const Pair& b, int i, int j, int k) {
+template <typename E>
+CACTO_D E bitonic_keep(const E& a, const E& b, int i, int j, int k) {
   const bool take_min = ((i & k) == 0) == ((i & j) == 0);
-  return (pair_less(b, a) == take_min) ? b : a;
+  return (elem_less(b, a) == take_min) ? b : a;
 }
 
-__global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(Pair* data, int64_t M) {
-  __shared__ Pair sh[kSortChunk];
+template <typename E>
+__global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(E* data, int64_t M) {
+  __shared__ E sh[kSortChunk];
   const int64_t base = (int64_t)blockIdx.x * kSortChunk;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int p0 = warp * 64 + lane, p1 = p0 + 32;
-  const Pair pad{~0ull, 0x7fffffffffffffffll};
-  Pair v0 = (base + p0 < M) ? data[base + p0] : pad;
-  Pair v1 = (base + p1 < M) ? data[base + p1] : pad;
+  E pad;
+  make_pad(pad);
+  E v0 = (base + p0 < M) ? data[base + p0] : pad;
+  E v1 = (base + p1 < M) ? data[base + p1] : pad;
   for (int k = 2; k <= kSortChunk; k <<= 1) {
     int j = k >> 1;
     for (; j >= 64; j >>= 1) {
       sh[p0] = v0;
       sh[p1] = v1;
       __syncthreads();
-      const Pair b0 = sh[p0 ^ j], b1 = sh[p1 ^ j];
+      const E b0 = sh[p0 ^ j], b1 = sh[p1 ^ j];
       __syncthreads();
       v0 = bitonic_keep(v0, b0, p0, j, k);
       v1 = bitonic_keep(v1, b1, p1, j, k);
     }
     if (j == 32) {
       const bool up = (p0 & k) == 0;
-      if (pair_less(v1, v0) == up) {
-        const Pair t = v0;
+      if (elem_less(v1, v0) == up) {
+        const E t = v0;
         v0 = v1;
         v1 = t;
       }
       j = 16;
     }
     for (; j > 0; j >>= 1) {
-      const Pair b0 = shfl_pair(v0, j), b1 = shfl_pair(v1, j);
+      const E b0 = shfl_elem(v0, j), b1 = shfl_elem(v1, j);
       v0 = bitonic_keep(v0, b0, p0, j, k);
       v1 = bitonic_keep(v1, b1, p1, j, k);
     }
@@ -260,7 +279,8 @@ __global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(Pair* data, in
 }
 
 // merge adjacent sorted runs of width w into runs of width 2w
-__global__ void merge_pass_kernel(const Pair* __restrict__ in, Pair* __restrict__ out, int64_t M, int64_t w) {
+template <typename E>
+__global__ void merge_pass_kernel(const E* __restrict__ in, E* __restrict__ out, int64_t M, int64_t w) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t run = i / w;
     int64_t pair_start = (run / 2) * 2 * w;
@@ -270,11 +290,11 @@ __global__ void merge_pass_kernel(const Pair* __restrict__ in, Pair* __restrict_
     int64_t o_end = left ? my_start + 2 * w : my_start;
     if (o_start > M) o_start = M;
     if (o_end > M) o_end = M;
-    Pair e = in[i];
+    const E e = in[i];
     int64_t lo = o_start, hi = o_end;  // count partner elements < e
     while (lo < hi) {
       int64_t mid = (lo + hi) >> 1;
-      if (pair_less(in[mid], e))
+      if (elem_less(in[mid], e))
         lo = mid + 1;
       else
         hi = mid;
@@ -283,13 +303,13 @@ __global__ void merge_pass_kernel(const Pair* __restrict__ in, Pair* __restrict_
   }
 }
 
-template <typename T>
-__global__ void emit_kernel(const Pair* __restrict__ sel, int64_t keep, int64_t base_index, int64_t* order,
+template <typename T, typename E>
+__global__ void emit_kernel(const E* __restrict__ sel, int64_t keep, int64_t base_index, int64_t* order,
                             T* top_scores) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < keep; i += (int64_t)gridDim.x * blockDim.x) {
-    Pair p = sel[i];
-    order[i] = p.idx + base_index;
-    if (top_scores) top_scores[i] = key_score(p.key, (T*)nullptr);
+    const E p = sel[i];
+    order[i] = elem_idx(p) + base_index;
+    if (top_scores) top_scores[i] = key_score(elem_key(p), (T*)nullptr);
   }
 }
 
@@ -302,20 +322,21 @@ __global__ void runs_to_pairs_kernel(const T* __restrict__ s, const int64_t* __r
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // sorts `M` pairs in a (ping-pong with b); returns the buffer holding the result
-static Pair* sort_pairs(Pair* a, Pair* b, int64_t M, int64_t first_width, cudaStream_t st) {
+template <typename E>
+static E* sort_pairs(E* a, E* b, int64_t M, int64_t first_width, cudaStream_t st) {
   int64_t w = first_width;
   if (w <= 0) {
     int64_t chunks = (M + kSortChunk - 1) / kSortChunk;
-    if (chunks > 0) chunk_sort_kernel<<<(unsigned)chunks, kSortThreads, 0, st>>>(a, M);
+    if (chunks > 0) chunk_sort_kernel<E><<<(unsigned)chunks, kSortThreads, 0, st>>>(a, M);
     w = kSortChunk;
   }
-  Pair* src = a;
-  Pair* dst = b;
+  E* src = a;
+  E* dst = b;
   while (w < M) {
     int64_t blocks = (M + 255) / 256;
     if (blocks > 4096) blocks = 4096;
-    merge_pass_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, dst, M, w);
-    Pair* t = src;
+    merge_pass_kernel<E><<<(unsigned)blocks, 256, 0, st>>>(src, dst, M, w);
+    E* t = src;
     src = dst;
     dst = t;
     w *= 2;
@@ -334,16 +355,16 @@ extern "C" size_t cacto_select_workspace_bytes(int32_t dtype, int64_t N, int64_t
   return align256(sizeof(SelState)) + 2 * align256((size_t)k * sizeof(Pair));
 }
 
-template <typename T>
-static int select_entry(const T* scores, int64_t N, int64_t keep, int64_t base_index, int64_t* order, T* top,
-                        void* ws, cudaStream_t st) {
+template <typename T, typename E>
+static int select_run(const T* scores, int64_t N, int64_t keep, int64_t base_index, int64_t* order, T* top,
+                      void* ws, cudaStream_t st) {
   SelState* state = (SelState*)ws;
-  Pair* a = (Pair*)((char*)ws + align256(sizeof(SelState)));
-  Pair* b = (Pair*)((char*)a + align256((size_t)keep * sizeof(Pair)));
+  E* a = (E*)((char*)ws + align256(sizeof(SelState)));
+  E* b = (E*)((char*)a + align256((size_t)keep * sizeof(E)));
   if (cudaMemsetAsync(state, 0, sizeof(SelState), st) != cudaSuccess)
     return set_error(CACTO_ECUDA, "select: memset failed");
   constexpr int KB = sizeof(T) == 4 ? 32 : 64;
-  auto kern = radix_select_kernel<T, KB>;
+  auto kern = radix_select_kernel<T, KB, E>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSelThreads, 0);
   if (occ < 1) occ = 1;
@@ -356,10 +377,18 @@ static int select_entry(const T* scores, int64_t N, int64_t keep, int64_t base_i
   void* args[] = {(void*)&scores, (void*)&N, (void*)&keep, (void*)&state, (void*)&a};
   if (cudaLaunchCooperativeKernel((void*)kern, G, kSelThreads, args, 0, st) != cudaSuccess)
     return check_launch("radix_select_kernel (cooperative)");
-  Pair* res = sort_pairs(a, b, keep, 0, st);
+  E* res = sort_pairs<E>(a, b, keep, 0, st);
   int64_t eb = (keep + 255) / 256;
-  emit_kernel<T><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, base_index, order, top);
+  emit_kernel<T, E><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, base_index, order, top);
   return check_launch("select emit");
+}
+
+template <typename T>
+static int select_entry(const T* scores, int64_t N, int64_t keep, int64_t base_index, int64_t* order, T* top,
+                        void* ws, cudaStream_t st) {
+  if (sizeof(T) == 4 && N <= 0xFFFFFFFFll)
+    return select_run<T, Packed>(scores, N, keep, base_index, order, top, ws, st);
+  return select_run<T, Pair>(scores, N, keep, base_index, order, top, ws, st);
 }
 
 extern "C" int cacto_select_topk(int32_t dtype, const void* scores, int64_t N, int64_t keep, int64_t base_index,
@@ -398,8 +427,8 @@ extern "C" int cacto_select_merge(int32_t dtype, const void* run_scores, const i
   Pair* res = sort_pairs(a, b, M, keep, st);
   int64_t eb = (keep + 255) / 256;
   if (dtype == CACTO_F32)
-    emit_kernel<float><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, 0, order, (float*)top_scores);
+    emit_kernel<float, Pair><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, 0, order, (float*)top_scores);
   else
-    emit_kernel<double><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, 0, order, (double*)top_scores);
+    emit_kernel<double, Pair><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, 0, order, (double*)top_scores);
   return check_launch("select_merge");
 }
