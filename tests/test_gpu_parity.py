@@ -587,3 +587,18 @@ def test_ring_push_wrap_and_gather_bitwise(prec, n, m, cap, pushes, bsz):
             np.testing.assert_array_equal(g.cpu().numpy().reshape(want.shape), want)
     finally:
         set_precision(old)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("R,N,K", [(200, 65536, 6553), (7, 100, 33), (64, 5000, 5000), (1, 3, 1)])
+def test_take_columns_bitwise(dtype, R, N, K):
+    """cacto_take_columns (kept warm starts out of K1's time-major U): dst[k, r] = src[r, idx[k]]."""
+    from paper_2602_19699_b200 import _lib
+    dt = torch.float32 if dtype == "f32" else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(R * 7 + K)
+    src = torch.randn((R, N), device="cuda", dtype=dt, generator=g)
+    idx = torch.randint(0, N, (K,), device="cuda", generator=g)
+    dst = torch.empty((K, R), device="cuda", dtype=dt)
+    _lib.call("cacto_take_columns", _lib.F32 if dtype == "f32" else _lib.F64, src.data_ptr(), R, N, idx.data_ptr(),
+              K, dst.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert torch.equal(dst, src[:, idx].T)
