@@ -172,11 +172,19 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
 
   // ordered count of equal keys in this block's chunk
   unsigned int my_eq = 0;
-  for (int64_t base = c0; base < c1; base += kSelThreads) {
-    int64_t i = base + tid;
-    bool eq = i < c1 && score_key(scores[i]) == kstar;
-    unsigned int b = __ballot_sync(0xffffffffu, eq);
-    if (lane == 0) my_eq += __popc(b);
+  for (int64_t b0 = c0; b0 < c1; b0 += kSelBatch * kSelThreads) {
+    T v[kSelBatch];
+#pragma unroll
+    for (int u = 0; u < kSelBatch; ++u) {
+      const int64_t i = b0 + u * kSelThreads + tid;
+      v[u] = i < c1 ? scores[i] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < kSelBatch; ++u) {
+      const bool eq = b0 + u * kSelThreads + tid < c1 && score_key(v[u]) == kstar;
+      unsigned int b = __ballot_sync(0xffffffffu, eq);
+      if (lane == 0) my_eq += __popc(b);
+    }
   }
   if (lane == 0) s_warp[warp] = my_eq;
   __syncthreads();
@@ -198,28 +206,42 @@ __global__ void __launch_bounds__(kSelThreads) radix_select_kernel(const T* __re
     __syncthreads();
   }
   long long running = s_off;
-  for (int64_t base = c0; base < c1; base += kSelThreads) {
-    int64_t i = base + tid;
-    unsigned long long k = i < c1 ? score_key(scores[i]) : ~0ull;
-    bool lt = i < c1 && k < kstar;
-    bool eq = i < c1 && k == kstar;
-    if (lt) {
-      unsigned long long slot = atomicAdd(&st->n_lt, 1ull);
-      make_elem(sel[slot], k, (long long)i);
+  for (int64_t b0 = c0; b0 < c1; b0 += kSelBatch * kSelThreads) {  // block-uniform trip count
+    unsigned long long kk[kSelBatch];
+#pragma unroll
+    for (int u = 0; u < kSelBatch; ++u) {
+      const int64_t i = b0 + u * kSelThreads + tid;
+      kk[u] = i < c1 ? score_key(scores[i]) : ~0ull;
     }
-    unsigned int b = __ballot_sync(0xffffffffu, eq);
-    if (lane == 0) s_warp[warp] = __popc(b);
-    __syncthreads();
-    long long woff = running;
-    for (int w = 0; w < warp; ++w) woff += s_warp[w];
-    unsigned int tot = 0;
-    for (int w = 0; w < kSelThreads / 32; ++w) tot += s_warp[w];
-    if (eq) {
-      long long r = woff + __popc(b & ((1u << lane) - 1u));
-      if (r < need_eq) make_elem(sel[n_lt_total + r], k, (long long)i);
+#pragma unroll
+    for (int u = 0; u < kSelBatch; ++u) {
+      const int64_t i = b0 + u * kSelThreads + tid;
+      const unsigned long long k = kk[u];
+      const bool lt = i < c1 && k < kstar;
+      const bool eq = i < c1 && k == kstar;
+      // keys < K*: any slot order (sorted afterwards); one atomic per warp
+      const unsigned int lb = __ballot_sync(0xffffffffu, lt);
+      if (lb) {
+        unsigned long long wbase = 0;
+        if (lane == 0) wbase = atomicAdd(&st->n_lt, (unsigned long long)__popc(lb));
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        if (lt) make_elem(sel[wbase + __popc(lb & ((1u << lane) - 1u))], k, (long long)i);
+      }
+      // keys == K*: the lowest-index need_eq of them, in index order
+      const unsigned int b = __ballot_sync(0xffffffffu, eq);
+      if (lane == 0) s_warp[warp] = __popc(b);
+      __syncthreads();
+      long long woff = running;
+      for (int w = 0; w < warp; ++w) woff += s_warp[w];
+      unsigned int tot = 0;
+      for (int w = 0; w < kSelThreads / 32; ++w) tot += s_warp[w];
+      if (eq) {
+        long long r = woff + __popc(b & ((1u << lane) - 1u));
+        if (r < need_eq) make_elem(sel[n_lt_total + r], k, (long long)i);
+      }
+      running += tot;
+      __syncthreads();
     }
-    running += tot;
-    __syncthreads();
   }
 }
 
