@@ -260,17 +260,11 @@ CACTO_D E bitonic_keep(const E& a, const E& b, int i, int j, int k) {
   return (elem_less(b, a) == take_min) ? b : a;
 }
 
+// ascending bitonic sort of S = 64..kSortChunk elements held two per thread
+// (S / 2 threads), `sh` is S elements of scratch
 template <typename E>
-__global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(E* data, int64_t M) {
-  __shared__ E sh[kSortChunk];
-  const int64_t base = (int64_t)blockIdx.x * kSortChunk;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int p0 = warp * 64 + lane, p1 = p0 + 32;
-  E pad;
-  make_pad(pad);
-  E v0 = (base + p0 < M) ? data[base + p0] : pad;
-  E v1 = (base + p1 < M) ? data[base + p1] : pad;
-  for (int k = 2; k <= kSortChunk; k <<= 1) {
+CACTO_D void bitonic_sort_regs(E& v0, E& v1, E* sh, int p0, int p1, int S) {
+  for (int k = 2; k <= S; k <<= 1) {
     int j = k >> 1;
     for (; j >= 64; j >>= 1) {
       sh[p0] = v0;
@@ -296,8 +290,46 @@ __global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(E* data, int64
       v1 = bitonic_keep(v1, b1, p1, j, k);
     }
   }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(kSortThreads) chunk_sort_kernel(E* data, int64_t M) {
+  __shared__ E sh[kSortChunk];
+  const int64_t base = (int64_t)blockIdx.x * kSortChunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p0 = warp * 64 + lane, p1 = p0 + 32;
+  E pad;
+  make_pad(pad);
+  E v0 = (base + p0 < M) ? data[base + p0] : pad;
+  E v1 = (base + p1 < M) ? data[base + p1] : pad;
+  bitonic_sort_regs(v0, v1, sh, p0, p1, kSortChunk);
   if (base + p0 < M) data[base + p0] = v0;
   if (base + p1 < M) data[base + p1] = v1;
+}
+
+// N <= kSortChunk candidates (e.g. the 750-start CPU-reference config): the whole
+// select in one CTA -- keys, one bitonic sort of all N pairs, emit the first keep
+template <typename T, typename E>
+__global__ void __launch_bounds__(kSortThreads) small_select_kernel(const T* __restrict__ scores, int N, int keep,
+                                                                     int64_t base_index, int64_t* order,
+                                                                     T* top_scores, int S) {
+  __shared__ E sh[kSortChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p0 = warp * 64 + lane, p1 = p0 + 32;
+  E v0, v1;
+  make_pad(v0);
+  make_pad(v1);
+  if (p0 < N) make_elem(v0, score_key(scores[p0]), p0);
+  if (p1 < N) make_elem(v1, score_key(scores[p1]), p1);
+  bitonic_sort_regs(v0, v1, sh, p0, p1, S);
+  if (p0 < keep) {
+    order[p0] = elem_idx(v0) + base_index;
+    if (top_scores) top_scores[p0] = key_score(elem_key(v0), (T*)nullptr);
+  }
+  if (p1 < keep) {
+    order[p1] = elem_idx(v1) + base_index;
+    if (top_scores) top_scores[p1] = key_score(elem_key(v1), (T*)nullptr);
+  }
 }
 
 // merge adjacent sorted runs of width w into runs of width 2w
@@ -380,6 +412,12 @@ extern "C" size_t cacto_select_workspace_bytes(int32_t dtype, int64_t N, int64_t
 template <typename T, typename E>
 static int select_run(const T* scores, int64_t N, int64_t keep, int64_t base_index, int64_t* order, T* top,
                       void* ws, cudaStream_t st) {
+  if (N <= kSortChunk) {
+    int S = 64;
+    while (S < N) S <<= 1;
+    small_select_kernel<T, E><<<1, S / 2, 0, st>>>(scores, (int)N, (int)keep, base_index, order, top, S);
+    return check_launch("small_select_kernel");
+  }
   SelState* state = (SelState*)ws;
   E* a = (E*)((char*)ws + align256(sizeof(SelState)));
   E* b = (E*)((char*)a + align256((size_t)keep * sizeof(E)));

@@ -170,7 +170,10 @@ class BicPipeline:
             launches += 3  # torch copy + fill of the augmented view, K2 score
             scores = score_device(self.mode, xa, self.std, self.critic, cost)
         order, top = select_topk_device(scores, keep, 0, self.ws)
-        launches += 4 + max(0, int(np.ceil(np.log2(max(keep, 1) / 2048.0))))  # memset, select, sort, merges, emit
+        if N <= 2048:
+            launches += 1  # single-CTA select (csrc/select.cu small_select_kernel)
+        else:
+            launches += 4 + max(0, int(np.ceil(np.log2(max(keep, 1) / 2048.0))))  # memset, select, sort, merges, emit
         out = {"order": order, "scores": top, "cost": cost}
         if warm_starts and keep > 0:
             T = self.model.t_max - t0

@@ -312,7 +312,8 @@ def test_select_ties_nan_signed_zero(precision):
     np.testing.assert_array_equal(order.cpu().numpy(), d["select_ties_order"])
 
 
-@pytest.mark.parametrize("N,keep", [(1, 1), (1000, 1000), (65536, 6553), (1 << 20, 104857), (300001, 7)])
+@pytest.mark.parametrize("N,keep", [(1, 1), (65, 3), (750, 75), (1000, 1000), (2048, 300), (2049, 2049), (65536, 6553),
+                                    (1 << 20, 104857), (300001, 7)])
 def test_select_large_with_heavy_ties(N, keep, precision):
     rng = np.random.default_rng(N)
     s = np.round(rng.normal(0, 1, N), 2)          # ~600 distinct values -> massive ties
@@ -321,7 +322,9 @@ def test_select_large_with_heavy_ties(N, keep, precision):
     dt = torch.float64 if precision == "fp64" else torch.float32
     ref_s = s.astype(np.float32) if precision == "fp32" else s
     order, top = B_trainer.select_topk_device(torch.as_tensor(ref_s).to("cuda", dt), keep)
-    np.testing.assert_array_equal(order.cpu().numpy(), np.argsort(-ref_s, kind="stable")[:keep])
+    want = np.argsort(-ref_s, kind="stable")[:keep]
+    np.testing.assert_array_equal(order.cpu().numpy(), want)
+    np.testing.assert_array_equal(top.cpu().numpy(), ref_s[want])  # NaN == NaN, -0.0 == 0.0
 
 
 def test_select_rejects_keep_too_large():
