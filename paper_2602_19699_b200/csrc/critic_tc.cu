@@ -609,29 +609,61 @@ static Plan2 plan2(int64_t B, int64_t P) {
   return p;
 }
 
-// T_l [64][17 or 65] -> gW_l (first cols) and gb_l (bias column); T_3 [1][65] -> w_3, b_3
+// T_l [64][17 or 65] -> gW_l (first cols) and gb_l (bias column); T_3 [1][65] -> w_3, b_3.
+// One thread per gradient entry over the concatenated segments (each entry gets
+// exactly one add, as before, so the result is unchanged): ~13 k independent
+// read-modify-writes spread over ~52 CTAs instead of 4 CTAs' serial loops.
 __global__ void scatter_grads_kernel(const float* __restrict__ T0, const float* __restrict__ T1,
                                      const float* __restrict__ T2, const float* __restrict__ T3, int cols0,
                                      float* slot, int64_t w0, int64_t b0, int64_t w1, int64_t b1, int64_t w2,
                                      int64_t b2, int64_t w3, int64_t b3) {
-  const int l = blockIdx.x;
-  if (l < 3) {
-    const float* T = l == 0 ? T0 : (l == 1 ? T1 : T2);
-    const int cols = l == 0 ? cols0 : HP, N = l == 0 ? 17 : 65, bc = l == 0 ? 16 : 64;
-    float* gw = slot + (l == 0 ? w0 : (l == 1 ? w1 : w2));
-    float* gbv = slot + (l == 0 ? b0 : (l == 1 ? b1 : b2));
-    for (int e = threadIdx.x; e < HP * cols; e += blockDim.x) gw[e] += T[(e / cols) * N + (e % cols)];
-    for (int m = threadIdx.x; m < HP; m += blockDim.x) gbv[m] += T[m * N + bc];
-  } else {
-    for (int c = threadIdx.x; c < HP; c += blockDim.x) slot[w3 + c] += T3[c];
-    if (threadIdx.x == 0) slot[b3] += T3[64];
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < HP * cols0) {
+    slot[w0 + e] += T0[(e / cols0) * 17 + (e % cols0)];
+    return;
   }
+  e -= HP * cols0;
+  if (e < HP) {
+    slot[b0 + e] += T0[e * 17 + 16];
+    return;
+  }
+  e -= HP;
+#pragma unroll
+  for (int l = 1; l < 3; ++l) {
+    const float* T = l == 1 ? T1 : T2;
+    if (e < HP * HP) {
+      slot[(l == 1 ? w1 : w2) + e] += T[(e / HP) * 65 + (e % HP)];
+      return;
+    }
+    e -= HP * HP;
+    if (e < HP) {
+      slot[(l == 1 ? b1 : b2) + e] += T[e * 65 + 64];
+      return;
+    }
+    e -= HP;
+  }
+  if (e < HP) {
+    slot[w3 + e] += T3[e];
+    return;
+  }
+  if (e == HP) slot[b3] += T3[64];
 }
+constexpr int scatter_items(int cols0) { return HP * cols0 + HP + 2 * (HP * HP + HP) + HP + 1; }
+
+// loss partials of the per-tile CTAs -> one value; a fixed strided order per
+// thread and a fixed shuffle / shared-memory tree (deterministic)
 __global__ void loss_fold_kernel(const float* __restrict__ part, int n, float* dst) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    float s = 0.f;
-    for (int i = 0; i < n; ++i) s += part[i];
-    *dst = s;
+  __shared__ float ws[8];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    *dst = t;
   }
 }
 
@@ -721,9 +753,9 @@ int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_bat
   rc = gemm_tf32(1, 65, (int)K2, a.V3, (K2 + 3) / 4 * 4, 1, a.UA[3], 1, 68, T[3], 65, 0, a.inv_denom, 3, gws, gwb,
                  st);
   if (rc) return rc;
-  scatter_grads_kernel<<<4, 256, 0, st>>>(T[0], T[1], T[2], T[3], lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1],
-                                          lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);
-  loss_fold_kernel<<<1, 32, 0, st>>>(a.lossp, grid, slot + lo.total);
+  scatter_grads_kernel<<<(ctc::scatter_items(lo.cols[0]) + 255) / 256, 256, 0, st>>>(
+      T[0], T[1], T[2], T[3], lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1], lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);
+  loss_fold_kernel<<<1, 256, 0, st>>>(a.lossp, grid, slot + lo.total);
   return check_launch("critic_tc reductions");
 }
 
