@@ -26,6 +26,9 @@ int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, con
               float* D, int64_t ldd, int accumulate, float alpha, int passes, void* ws, size_t ws_bytes,
               cudaStream_t st);
 size_t gemm_workspace_bytes(int M, int N, int K);
+int gemm_tf32_partials(int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn,
+                       int64_t sbk, float alpha, int passes, void* ws, size_t ws_bytes, int* splits_out,
+                       cudaStream_t st);
 
 namespace ctc {
 
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
 namespace ctc {
 
 struct Plan2 {  // workspace carve
-  size_t off_gz[3], off_ua[4], off_v3, off_t[4], off_lossp, off_gemm, total;
+  size_t off_gz[3], off_ua[4], off_v3, off_lossp, off_part[4], part_bytes[4], total;
 };
 
 static Plan2 plan2(int64_t B, int64_t P) {
@@ -600,55 +603,67 @@ static Plan2 plan2(int64_t B, int64_t P) {
   p.off_ua[0] = take((size_t)2 * B * 20 * 4);
   for (int l = 1; l < 4; ++l) p.off_ua[l] = take((size_t)2 * B * 68 * 4);
   p.off_v3 = take((size_t)2 * B * 4 + 16);
-  for (int l = 0; l < 4; ++l) p.off_t[l] = take((size_t)HP * 68 * 4);
   p.off_lossp = take((size_t)4096 * 4);
-  size_t g = gemm_workspace_bytes(HP, 65, (int)(2 * B));
-  size_t g2 = gemm_workspace_bytes(1, 65, (int)(2 * B));
-  p.off_gemm = take(g > g2 ? g : g2);
+  // split-K partials of the four reduction GEMMs, each in its own region (the fused
+  // reduce + scatter reads all four after the last GEMM)
+  const int pm[4] = {HP, HP, HP, 1}, pn[4] = {17, 65, 65, 65};
+  for (int l = 0; l < 4; ++l) {
+    const size_t w = gemm_workspace_bytes(pm[l], pn[l], (int)(2 * B));
+    const size_t one = (size_t)pm[l] * pn[l] * 4;
+    p.part_bytes[l] = w > one ? w : one;
+    p.off_part[l] = take(p.part_bytes[l]);
+  }
   p.total = o + 256;
   return p;
 }
 
-// T_l [64][17 or 65] -> gW_l (first cols) and gb_l (bias column); T_3 [1][65] -> w_3, b_3.
-// One thread per gradient entry over the concatenated segments (each entry gets
-// exactly one add, as before, so the result is unchanged): ~13 k independent
-// read-modify-writes spread over ~52 CTAs instead of 4 CTAs' serial loops.
-__global__ void scatter_grads_kernel(const float* __restrict__ T0, const float* __restrict__ T1,
-                                     const float* __restrict__ T2, const float* __restrict__ T3, int cols0,
-                                     float* slot, int64_t w0, int64_t b0, int64_t w1, int64_t b1, int64_t w2,
-                                     int64_t b2, int64_t w3, int64_t b3) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < HP * cols0) {
-    slot[w0 + e] += T0[(e / cols0) * 17 + (e % cols0)];
-    return;
-  }
-  e -= HP * cols0;
-  if (e < HP) {
-    slot[b0 + e] += T0[e * 17 + 16];
-    return;
-  }
-  e -= HP;
-#pragma unroll
-  for (int l = 1; l < 3; ++l) {
-    const float* T = l == 1 ? T1 : T2;
-    if (e < HP * HP) {
-      slot[(l == 1 ? w1 : w2) + e] += T[(e / HP) * 65 + (e % HP)];
-      return;
-    }
-    e -= HP * HP;
-    if (e < HP) {
-      slot[(l == 1 ? b1 : b2) + e] += T[e * 65 + 64];
-      return;
-    }
-    e -= HP;
-  }
-  if (e < HP) {
-    slot[w3 + e] += T3[e];
-    return;
-  }
-  if (e == HP) slot[b3] += T3[64];
-}
+// gradient entries of the four reduction outputs: W_0 [64][cols0], b_0, W_1, b_1, W_2, b_2, w_3 [64], b_3
 constexpr int scatter_items(int cols0) { return HP * cols0 + HP + 2 * (HP * HP + HP) + HP + 1; }
+
+// split-K reduction fused with the scatter: one warp per gradient entry, lanes
+// over the splits and the fixed shuffle tree of tc::splitk_reduce_warp_kernel
+// (same sums, same order), lane 0 adds into the gradient slot -- one launch
+// instead of four reductions + a scatter
+struct PartSet {
+  const float* p[4];
+  int splits[4];
+  int64_t stride[4];
+};
+CACTO_D float split_sum(const PartSet& ps, int l, int64_t off, int lane) {
+  float s = 0.f;
+  for (int z = lane; z < ps.splits[l]; z += 32) s += ps.p[l][z * ps.stride[l] + off];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+__global__ void reduce_scatter_grads_kernel(const PartSet ps, int cols0, float* slot, int64_t w0, int64_t b0,
+                                            int64_t w1, int64_t b1, int64_t w2, int64_t b2, int64_t w3, int64_t b3) {
+  const int lane = threadIdx.x & 31;
+  int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // warp-uniform
+  int l;
+  int64_t off, dst;
+  if (e < HP * cols0) {
+    l = 0, off = (e / cols0) * 17 + (e % cols0), dst = w0 + e;
+  } else if ((e -= HP * cols0) < HP) {
+    l = 0, off = e * 17 + 16, dst = b0 + e;
+  } else if ((e -= HP) < HP * HP) {
+    l = 1, off = (e / HP) * 65 + (e % HP), dst = w1 + e;
+  } else if ((e -= HP * HP) < HP) {
+    l = 1, off = e * 65 + 64, dst = b1 + e;
+  } else if ((e -= HP) < HP * HP) {
+    l = 2, off = (e / HP) * 65 + (e % HP), dst = w2 + e;
+  } else if ((e -= HP * HP) < HP) {
+    l = 2, off = e * 65 + 64, dst = b2 + e;
+  } else if ((e -= HP) < HP) {
+    l = 3, off = e, dst = w3 + e;
+  } else if ((e -= HP) == 0) {
+    l = 3, off = 64, dst = b3;
+  } else {
+    return;
+  }
+  const float s = split_sum(ps, l, off, lane);
+  if (lane == 0) slot[dst] += s;
+}
 
 // loss partials of the per-tile CTAs -> one value; a fixed strided order per
 // thread and a fixed shuffle / shared-memory tree (deterministic)
@@ -738,23 +753,25 @@ int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_bat
   // from the bias column, the bias gradient; the output row w_3 and b_3 from a
   // 1-row GEMM with the [1 ; -2 e_v] factor.  Results (scaled by 1/denom) land in
   // small [rows][N] tiles that one kernel adds into the padded gradient slot.
-  void* gws = w + p.off_gemm;
-  const size_t gwb = p.total - p.off_gemm - 256;
   const int ncol[4] = {17, 65, 65, 65};
   const int wpad[4] = {20, 68, 68, 68};
-  float* T[4];
-  for (int l = 0; l < 4; ++l) T[l] = (float*)(w + p.off_t[l]);
+  ctc::PartSet ps{};
   for (int l = 0; l < 3; ++l) {
-    rc = gemm_tf32(HP, ncol[l], (int)(2 * B), a.GZ[l], 1, HP, a.UA[l], 1, wpad[l], T[l], ncol[l], 0, a.inv_denom, 3,
-                   gws, gwb, st);
+    ps.p[l] = (const float*)(w + p.off_part[l]);
+    ps.stride[l] = (int64_t)HP * ncol[l];
+    rc = gemm_tf32_partials(HP, ncol[l], (int)(2 * B), a.GZ[l], 1, HP, a.UA[l], 1, wpad[l], a.inv_denom, 3,
+                            w + p.off_part[l], p.part_bytes[l], &ps.splits[l], st);
     if (rc) return rc;
   }
   const int64_t K2 = 2 * B;
-  rc = gemm_tf32(1, 65, (int)K2, a.V3, (K2 + 3) / 4 * 4, 1, a.UA[3], 1, 68, T[3], 65, 0, a.inv_denom, 3, gws, gwb,
-                 st);
+  ps.p[3] = (const float*)(w + p.off_part[3]);
+  ps.stride[3] = 65;
+  rc = gemm_tf32_partials(1, 65, (int)K2, a.V3, (K2 + 3) / 4 * 4, 1, a.UA[3], 1, 68, a.inv_denom, 3,
+                          w + p.off_part[3], p.part_bytes[3], &ps.splits[3], st);
   if (rc) return rc;
-  scatter_grads_kernel<<<(ctc::scatter_items(lo.cols[0]) + 255) / 256, 256, 0, st>>>(
-      T[0], T[1], T[2], T[3], lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1], lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);
+  const int items = ctc::scatter_items(lo.cols[0]);
+  ctc::reduce_scatter_grads_kernel<<<(items * 32 + 255) / 256, 256, 0, st>>>(
+      ps, lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1], lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);
   loss_fold_kernel<<<1, 256, 0, st>>>(a.lossp, grid, slot + lo.total);
   return check_launch("critic_tc reductions");
 }

@@ -413,9 +413,12 @@ size_t gemm_workspace_bytes(int M, int N, int K) {
   return splits > 1 ? (size_t)splits * M * N * 4 : 0;
 }
 
-int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk,
-              float* D, int64_t ldd, int accumulate, float alpha, int passes, void* ws, size_t ws_bytes,
-              cudaStream_t st) {
+// partials_only: always write the per-split partial products [splits][M][N] into
+// ws (splits reported in *splits_out) and skip the split-K reduction -- for callers
+// that fuse the reduction into their own consumer (critic_tc's gradient scatter)
+static int gemm_tf32_impl(int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn,
+                          int64_t sbk, float* D, int64_t ldd, int accumulate, float alpha, int passes, void* ws,
+                          size_t ws_bytes, cudaStream_t st, bool partials_only, int* splits_out) {
   if (M <= 0 || N <= 0) return CACTO_OK;
   const int bn = tile_bn(N);
   CUtensorMap ma, mb;
@@ -433,10 +436,13 @@ int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, con
   const int nkb = (K + tc::BK - 1) / tc::BK;
   int splits = choose_splits(tiles, nkb);
   if (splits > 1 && (!ws || ws_bytes < (size_t)splits * M * N * 4)) splits = 1;
+  if (partials_only && (!ws || ws_bytes < (size_t)M * N * 4))
+    return set_error(CACTO_EVALUE, "gemm: partials workspace too small");
   g.kb_per_split = (nkb + splits - 1) / splits;
   if (g.kb_per_split > 0) splits = (nkb + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
   g.alpha = alpha;
-  if (splits > 1) {
+  if (splits_out) *splits_out = splits;
+  if (splits > 1 || partials_only) {
     g.D = (float*)ws;
     g.ldd = N;
     g.accumulate = 0;
@@ -451,7 +457,7 @@ int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, con
        : bn == 96  ? tc::launch_gemm<96>(ma, mb, g, splits, st)
        : bn == 128 ? tc::launch_gemm<128>(ma, mb, g, splits, st)
                    : tc::launch_gemm<256>(ma, mb, g, splits, st);
-  if (rc || splits == 1) return rc;
+  if (rc || splits == 1 || partials_only) return rc;
   int64_t total = (int64_t)M * N;
   unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 8 * num_sms());
   if (splits >= 16 && total < 65536) {  // few outputs: lanes over splits; else coalesced per element
@@ -463,6 +469,20 @@ int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, con
   }
   tc::splitk_reduce_kernel<<<grid, 256, 0, st>>>((const float*)ws, splits, (int64_t)M * N, M, N, N, D, ldd, accumulate);
   return check_launch("splitk_reduce_kernel");
+}
+
+int gemm_tf32(int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk,
+              float* D, int64_t ldd, int accumulate, float alpha, int passes, void* ws, size_t ws_bytes,
+              cudaStream_t st) {
+  return gemm_tf32_impl(M, N, K, A, sam, sak, B, sbn, sbk, D, ldd, accumulate, alpha, passes, ws, ws_bytes, st,
+                        false, nullptr);
+}
+
+int gemm_tf32_partials(int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn,
+                       int64_t sbk, float alpha, int passes, void* ws, size_t ws_bytes, int* splits_out,
+                       cudaStream_t st) {
+  return gemm_tf32_impl(M, N, K, A, sam, sak, B, sbn, sbk, nullptr, 0, 0, alpha, passes, ws, ws_bytes, st, true,
+                        splits_out);
 }
 
 
