@@ -333,21 +333,41 @@ static int make_map(CUtensorMap* map, const float* X, int rows, int K, int64_t s
 }
 
 // shared-memory stages: 3 at BN <= 128 (64 KB each), 2 at BN = 256 (96 KB each)
-template <int BN>
-static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmArgs g, int splits, cudaStream_t st) {
+// narrow tiles (BN <= 64) run two CTAs per SM with two stages each (2 x 97 KB
+// smem, 2 x 128 TMEM columns): two independent TMA -> split -> MMA chains per SM.
+// (BN = 96 does not fit twice: 2 x (113 KB + 1 KB reserved) > 228 KB)
+inline bool pair_ctas(int bn) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("CACTO_GEMM_PAIR");
+    env = e ? atoi(e) : 1;
+  }
+  return env != 0 && bn <= 64;
+}
+inline int cta_slots(int bn) { return (pair_ctas(bn) ? 2 : 1) * num_sms(); }
+
+template <int BN, int kStages>
+static int launch_gemm_k(const CUtensorMap& ma, const CUtensorMap& mb, GemmArgs g, int splits, int slots,
+                         cudaStream_t st) {
   constexpr uint32_t STAGE_BYTES = 2 * BM * BK * 4 + 2 * BN * BK * 4;
-  constexpr int kStages = BN >= 256 ? 2 : 3;
   const size_t smem = kStages * STAGE_BYTES + 1024;
   auto kern = gemm_tf32_kernel<BN, kStages>;
   if (!ensure_smem((const void*)kern, smem)) return set_error(CACTO_ECUDA, "gemm: %zu B smem unavailable", smem);
   g.mtiles = (g.M + BM - 1) / BM;
   g.ntiles = (g.N + BN - 1) / BN;
   g.splits = splits;
-  // persistent: one CTA per SM walks the tiles (double-buffered TMEM accumulator)
+  // persistent: one CTA per slot walks the tiles (double-buffered TMEM accumulator)
   const int64_t tiles = (int64_t)g.mtiles * g.ntiles * splits;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, slots);
   kern<<<grid, kThreadsTC, smem, st>>>(ma, mb, g);
   return check_launch("gemm_tf32_kernel");
+}
+template <int BN>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmArgs g, int splits, cudaStream_t st) {
+  if constexpr (BN <= 64) {
+    if (pair_ctas(BN)) return launch_gemm_k<BN, 2>(ma, mb, g, splits, cta_slots(BN), st);
+  }
+  return launch_gemm_k<BN, BN >= 256 ? 2 : 3>(ma, mb, g, splits, num_sms(), st);
 }
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int M, int N,
@@ -394,9 +414,9 @@ static int tile_bn(int N) {
 // split-K when the tile grid cannot fill the GPU and K is long (weight gradients):
 // as many splits as fill the SMs (not only powers of two), >= 8 k-blocks each,
 // never an empty split
-static int choose_splits(int tiles, int nkb) {
-  if (tiles * 2 > num_sms()) return 1;
-  int splits = std::max(1, std::min(num_sms() / tiles, nkb / 8));
+static int choose_splits(int tiles, int nkb, int slots) {
+  if (tiles * 2 > slots) return 1;
+  int splits = std::max(1, std::min(slots / tiles, nkb / 8));
   if (splits > 1) {
     const int per = (nkb + splits - 1) / splits;
     splits = (nkb + per - 1) / per;
@@ -409,7 +429,7 @@ size_t gemm_workspace_bytes(int M, int N, int K) {
   const int bn = tile_bn(N);
   const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + bn - 1) / bn);
   const int nkb = (K + tc::BK - 1) / tc::BK;
-  const int splits = choose_splits(tiles, nkb);
+  const int splits = choose_splits(tiles, nkb, tc::cta_slots(bn));
   return splits > 1 ? (size_t)splits * M * N * 4 : 0;
 }
 
@@ -434,7 +454,7 @@ static int gemm_tf32_impl(int M, int N, int K, const float* A, int64_t sam, int6
   // split-K when the tile grid cannot fill the GPU and K is long (weight gradients)
   const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + bn - 1) / bn);
   const int nkb = (K + tc::BK - 1) / tc::BK;
-  int splits = choose_splits(tiles, nkb);
+  int splits = choose_splits(tiles, nkb, tc::cta_slots(bn));
   if (splits > 1 && (!ws || ws_bytes < (size_t)splits * M * N * 4)) splits = 1;
   if (partials_only && (!ws || ws_bytes < (size_t)M * N * 4))
     return set_error(CACTO_EVALUE, "gemm: partials workspace too small");
