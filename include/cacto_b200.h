@@ -146,11 +146,16 @@ int cacto_mlp_jacobian(const cacto_mlp_t* mlp, const void* xa, int64_t B, void* 
 
 /* -- (a1-a5) closed-loop rollout: nets.actor_rollout, nets.py:403-423 -------
  * x0 [N, n] float64 host-API layout (device pointer), start times t0 [N] int32
- * (or NULL -> t0_scalar for all), horizon t_hor (<= t_max - t0, else
- * CACTO_EVALUE like nets.py:409-410).  Outputs (dtype, each optional/NULL):
- *   U [N, t_hor, m], X [N, t_hor+1, n], step_costs [N, t_hor+1], cost [N]
+ * (or NULL -> t0_scalar for all), horizon t_hor >= 0 (<= t_max - t0, else
+ * CACTO_EVALUE like nets.py:409-410; t_hor = 0 gives the reference's 1-row
+ * trajectory), or CACTO_FULL_HORIZON: every start runs to its own horizon
+ * t_max - t0[i] and the output row stride is t_max (rows past a start's
+ * horizon are left untouched).  Outputs (dtype, each optional/NULL), with
+ * S = t_hor (or t_max for CACTO_FULL_HORIZON):
+ *   U [N, S, m], X [N, S+1, n], step_costs [N, S+1], cost [N]
  * Costs need `cost` != NULL (field given); without a field step costs are 0.
  * cost[i] = NumPy pairwise sum of step_costs[i] (Trajectory.cost, ilqr.py:76-78). */
+enum { CACTO_FULL_HORIZON = -1 };
 int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
                   const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
                   void* U, void* X, void* step_costs, void* cost_to_go, void* stream);
@@ -198,6 +203,34 @@ int cacto_select_topk(int32_t dtype, const void* scores, int64_t N, int64_t keep
 int cacto_select_merge(int32_t dtype, const void* run_scores, const int64_t* run_index, int32_t R,
                        int64_t keep, int64_t* order, void* top_scores, void* workspace,
                        size_t workspace_bytes, void* stream);
+
+/* -- (a6 over shards) distributed stable top-k: the union of all
+ * ranks' contiguous candidate shards selected exactly like trainer.py:152, with
+ * only a 2 KB histogram per digit, 16 B of counts per rank and the keep_global
+ * winners crossing ranks.  The caller runs the collectives between the phases
+ * (paper_2602_19699_b200.parallel.distributed_select):
+ *   begin; for pass in 0..(32|64)/8-1: pass -> hist (local, [256] int64)
+ *          -> all-reduce SUM -> digit(hist_global) ;
+ *   after the last digit counts = {lt_local, eq_local, need} -> all-gather (lt, eq);
+ *   host: take_r = clamp(need - sum_{q<r} eq_q, 0, eq_r), c_r = lt_r + take_r,
+ *         offset_r = sum_{q<r} c_q ;
+ *   local(n_candidates = lt_r + eq_r, n_take = c_r, offset_r): the rank's winners
+ *         into elements [offset_r, offset_r + c_r) of a ZEROED keep_global-element
+ *         buffer (fp32: one int64 per element; fp64: two) and their local indices
+ *         (rank-local order = global order) -> all-reduce SUM of the buffer ->
+ *   finish: global order [keep_global] (+ scores) on every rank. */
+size_t cacto_dselect_workspace_bytes(int32_t dtype, int64_t N_local, int64_t keep);
+int cacto_dselect_begin(int32_t dtype, int64_t N_local, int64_t keep, int64_t keep_global, void* workspace,
+                        size_t workspace_bytes, void* stream);
+int cacto_dselect_pass(int32_t dtype, const void* scores, int64_t N_local, int64_t keep, int32_t pass,
+                       void* workspace, int64_t* hist_out, void* stream);
+int cacto_dselect_digit(int32_t dtype, int64_t N_local, int64_t keep, int32_t pass, const int64_t* hist_global,
+                        void* workspace, int64_t* counts, void* stream);
+int cacto_dselect_local(int32_t dtype, const void* scores, int64_t N_local, int64_t keep, int64_t base_index,
+                        int64_t n_candidates, int64_t n_take, int64_t offset, void* workspace, void* global_elems,
+                        int64_t* local_sel, void* stream);
+int cacto_dselect_finish(int32_t dtype, void* global_elems, int64_t keep_global, int64_t* order, void* top_scores,
+                         void* scratch, size_t scratch_bytes, void* stream);
 
 /* -- (a17) replay gather: ReplayBuffer.sample_minibatch, buffer.py:132-138 --
  * out columns get rows idx[b] of the ring columns (batch->idx required). */

@@ -80,6 +80,7 @@ _PBATCH = ctypes.POINTER(CactoBatch)
 _PI32 = ctypes.POINTER(ctypes.c_int32)
 
 ROLLOUT_U_TIME_MAJOR = 1   # CACTO_ROLLOUT_U_TIME_MAJOR
+FULL_HORIZON = -1          # CACTO_FULL_HORIZON
 
 # symbol -> (restype, argtypes); mirrors include/cacto_b200.h one to one
 SIGNATURES = {
@@ -99,6 +100,12 @@ SIGNATURES = {
     "cacto_select_workspace_bytes": (_SZ, [_I32, _I64, _I64]),
     "cacto_select_topk": (ctypes.c_int, [_I32, _P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "cacto_select_merge": (ctypes.c_int, [_I32, _P, _P, _I32, _I64, _P, _P, _P, _SZ, _P]),
+    "cacto_dselect_workspace_bytes": (_SZ, [_I32, _I64, _I64]),
+    "cacto_dselect_begin": (ctypes.c_int, [_I32, _I64, _I64, _I64, _P, _SZ, _P]),
+    "cacto_dselect_pass": (ctypes.c_int, [_I32, _P, _I64, _I64, _I32, _P, _P, _P]),
+    "cacto_dselect_digit": (ctypes.c_int, [_I32, _I64, _I64, _I32, _P, _P, _P, _P]),
+    "cacto_dselect_local": (ctypes.c_int, [_I32, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "cacto_dselect_finish": (ctypes.c_int, [_I32, _P, _I64, _P, _P, _P, _SZ, _P]),
     "cacto_gather": (ctypes.c_int, [_PBATCH, _P, _P, _P, _P, _P, _P]),
     "cacto_ring_push": (ctypes.c_int, [_PBATCH, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "cacto_kstep_push": (ctypes.c_int, [ctypes.POINTER(CactoSolutions), _I32, _I32, _P, _P, _P, _P, _P, _I64, _I64,

@@ -52,7 +52,7 @@ rollout_kernel(const RolloutArgs<T> a) {
 #pragma unroll
     for (int c = 0; c < n; ++c) x[c] = (T)a.x0[gi * n + c];
     t0 = a.t0 ? a.t0[gi] : a.t0_scalar;
-    T_i = a.t_hor > 0 ? a.t_hor : (a.sys.t_max - t0);
+    T_i = a.t_hor >= 0 ? a.t_hor : (a.sys.t_max - t0);
     acc.init(T_i + 1);
     if (a.X) {
 #pragma unroll
@@ -239,11 +239,11 @@ extern "C" int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* c
   if (actor->sizes[0] != sys->n + 1 || actor->sizes[actor->n_layers] != sys->m)
     return set_error(CACTO_EVALUE, "rollout: actor dims [%d -> %d] do not match system (n=%d, m=%d)",
                      actor->sizes[0], actor->sizes[actor->n_layers], sys->n, sys->m);
-  if (t_hor < 0) return set_error(CACTO_EVALUE, "rollout: negative horizon");
-  if (!t0 && t_hor > sys->t_max - t0_scalar)
+  if (t_hor < CACTO_FULL_HORIZON) return set_error(CACTO_EVALUE, "rollout: negative horizon %d", t_hor);
+  if (!t0 && (t_hor > sys->t_max - t0_scalar || t0_scalar > sys->t_max))
     return set_error(CACTO_EVALUE, "rollout of %d steps exceeds horizon from t=%d", t_hor, t0_scalar);
   if (N == 0) return CACTO_OK;
-  int stride = t_hor > 0 ? t_hor : sys->t_max;
+  int stride = t_hor >= 0 ? t_hor : sys->t_max;
   cudaStream_t st = (cudaStream_t)stream;
   NetShape sh = shape_of(*actor);
   if (actor->dtype == CACTO_F32) {
@@ -318,7 +318,7 @@ extern "C" int cacto_rollout_score(const cacto_system_t* sys, const cacto_cost_t
   a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
   a.params = (const float*)actor->params;
   a.x0 = x0; a.t0 = nullptr; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor;
-  a.t_stride = t_hor > 0 ? t_hor : sys->t_max;
+  a.t_stride = t_hor;
   a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : 0;
   a.U = (float*)U; a.C = (float*)cost_to_go;
   if (need_std) {

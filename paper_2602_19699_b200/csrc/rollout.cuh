@@ -19,7 +19,7 @@ struct RolloutArgs {
   const int32_t* t0;
   int t0_scalar;
   int64_t N;
-  int t_hor;      // > 0 fixed horizon; 0 -> per-start t_max - t0
+  int t_hor;      // >= 0 fixed horizon; CACTO_FULL_HORIZON (-1) -> per-start t_max - t0
   int t_stride;   // row stride of the per-step outputs
   int u_tmajor;   // U as [t_hor][m][N] (CACTO_ROLLOUT_U_TIME_MAJOR)
   CACTO_D int64_t u_at(int64_t gi, int k, int j, int m) const {

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
 #pragma unroll
     for (int c = 0; c < n; ++c) x[c] = (float)a.x0[gi * n + c];
     t0 = a.t0 ? a.t0[gi] : a.t0_scalar;
-    T_i = a.t_hor > 0 ? a.t_hor : (a.sys.t_max - t0);
+    T_i = a.t_hor >= 0 ? a.t_hor : (a.sys.t_max - t0);
     acc.init(T_i + 1, acc_s);
     if (a.X) {
 #pragma unroll

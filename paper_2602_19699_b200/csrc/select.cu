@@ -345,10 +345,14 @@ __global__ void merge_pass_kernel(const E* __restrict__ in, E* __restrict__ out,
     if (o_start > M) o_start = M;
     if (o_end > M) o_end = M;
     const E e = in[i];
-    int64_t lo = o_start, hi = o_end;  // count partner elements < e
+    // stable merge: a left-run element goes before equal right-run elements, so it
+    // counts the partner elements < e and a right-run element those <= e (equal
+    // elements, e.g. the padding pairs of several shards, land in distinct slots)
+    int64_t lo = o_start, hi = o_end;
     while (lo < hi) {
       int64_t mid = (lo + hi) >> 1;
-      if (elem_less(in[mid], e))
+      const E p = in[mid];
+      if (left ? elem_less(p, e) : !elem_less(e, p))
         lo = mid + 1;
       else
         hi = mid;
@@ -491,4 +495,252 @@ extern "C" int cacto_select_merge(int32_t dtype, const void* run_scores, const i
   else
     emit_kernel<double, Pair><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, keep, 0, order, (double*)top_scores);
   return check_launch("select_merge");
+}
+
+// ---------------------------------------------------------------------------------
+// Distributed stable top-k over contiguous shards (trainer.py:152
+// over the union of every rank's candidates).  The host sequences the phases and
+// runs the collectives between them (python: parallel.distributed_select):
+//   begin                         zero the state
+//   for each 8-bit digit (MSB first):
+//     pass   -> local 256-bin histogram of the digit among keys matching the prefix
+//     [all-reduce SUM of the histogram, 2 KB]
+//     digit  -> the digit where the global cumulative count reaches the still-needed
+//               k; prefix, k and this rank's count of keys < prefix updated
+//   counts -> (lt_local, eq_local) of the final threshold key K*
+//   [all-gather of (lt, eq), 16 B per rank]     host: take_r, offset_r (rank order =
+//               global index order, so ties at K* go to the lowest ranks first)
+//   compact -> every local key <= K* as (key, global index) elements
+//   [sort]  -> the rank's winners: the first lt_r + take_r sorted elements, written
+//               into its [offset_r, offset_r + c_r) segment of a zeroed keep-row buffer
+//               and their LOCAL indices (the rank's own kept rows, for the warm starts)
+//   [all-reduce SUM of the keep-row buffer: disjoint segments -> concatenation]
+//   finish  -> sort of the keep elements -> global order + scores on every rank
+// Only the threshold histograms, the counts and the keep winners cross ranks.
+// ---------------------------------------------------------------------------------
+namespace cacto {
+
+struct DSelState {
+  unsigned long long prefix, mask;
+  long long need;       // global count still needed among keys matching the prefix
+  long long lt_local;   // this rank's keys < prefix (decided digits)
+  long long eq_local;   // this rank's keys == K* (after the last pass)
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) dsel_hist_kernel(const T* __restrict__ scores, int64_t N, int shift,
+                                                        const DSelState* __restrict__ st, long long* hist) {
+  __shared__ unsigned int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned long long prefix = st->prefix, mask = st->mask;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = score_key(scores[i]);
+    if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd((unsigned long long*)&hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+}
+
+// one CTA of 256 threads: inclusive scan of the global histogram, pick the digit
+__global__ void __launch_bounds__(256) dsel_digit_kernel(const long long* __restrict__ hist_local,
+                                                         const long long* __restrict__ hist_global, int shift,
+                                                         int last, DSelState* st, long long* counts) {
+  __shared__ long long sg[256], sl[256];
+  const int t = threadIdx.x;
+  sg[t] = hist_global[t];
+  sl[t] = hist_local[t];
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {  // Hillis-Steele inclusive scans
+    long long a = t >= o ? sg[t - o] : 0, b = t >= o ? sl[t - o] : 0;
+    __syncthreads();
+    sg[t] += a;
+    sl[t] += b;
+    __syncthreads();
+  }
+  const long long need = st->need;
+  const long long before = t ? sg[t - 1] : 0;
+  if (before < need && need <= sg[t]) {  // exactly one digit qualifies
+    st->need = need - before;
+    st->prefix |= (unsigned long long)t << shift;
+    st->mask |= 255ull << shift;
+    st->lt_local += t ? sl[t - 1] : 0;
+    const long long eq = sl[t] - (t ? sl[t - 1] : 0);
+    if (last) {
+      st->eq_local = eq;
+      counts[0] = st->lt_local;
+      counts[1] = eq;
+      counts[2] = st->need;  // keys == K* to take, over all ranks
+    }
+  }
+}
+
+template <typename T, typename E>
+__global__ void dsel_compact_kernel(const T* __restrict__ scores, int64_t N, int64_t base,
+                                    const DSelState* __restrict__ st, E* out, unsigned long long* cursor) {
+  const unsigned long long K = st->prefix;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    unsigned long long k = ~0ull;
+    if (i < N) k = score_key(scores[i]);
+    const bool take = i < N && k <= K;
+    const unsigned int ball = __ballot_sync(0xffffffffu, take);
+    unsigned long long w = 0;
+    if (lane == 0 && ball) w = atomicAdd(cursor, (unsigned long long)__popc(ball));
+    w = __shfl_sync(0xffffffffu, w, 0);
+    if (take) {
+      E e;
+      make_elem(e, k, base + i);
+      out[w + __popc(ball & ((1u << lane) - 1u))] = e;
+    }
+  }
+}
+
+// first c sorted elements -> global segment [off, off + c) and local indices
+template <typename E>
+__global__ void dsel_emit_local_kernel(const E* __restrict__ sorted, int64_t c, int64_t base, int64_t off,
+                                       E* global, int64_t* local_sel) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c; i += (int64_t)gridDim.x * blockDim.x) {
+    const E e = sorted[i];
+    global[off + i] = e;
+    if (local_sel) local_sel[i] = elem_idx(e) - base;
+  }
+}
+
+static size_t dsel_elem_bytes(int32_t dtype) { return dtype == CACTO_F32 ? sizeof(Packed) : sizeof(Pair); }
+
+}  // namespace cacto
+
+extern "C" size_t cacto_dselect_workspace_bytes(int32_t dtype, int64_t N_local, int64_t keep) {
+  const size_t eb = dsel_elem_bytes(dtype);
+  const int64_t M = (N_local > keep ? N_local : keep) + 1;
+  // state | cursor | 8 x 256 local hist | 2 x M elements (sort ping-pong)
+  return align256(sizeof(DSelState)) + align256(sizeof(unsigned long long)) + align256(8 * 256 * sizeof(long long)) +
+         2 * align256((size_t)M * eb);
+}
+
+struct DselWs {
+  DSelState* st;
+  unsigned long long* cursor;
+  long long* hist;
+  char* a;
+  char* b;
+};
+
+static DselWs dsel_ws(void* ws, int32_t dtype, int64_t N_local, int64_t keep) {
+  DselWs w;
+  char* p = (char*)ws;
+  w.st = (DSelState*)p;
+  p += align256(sizeof(DSelState));
+  w.cursor = (unsigned long long*)p;
+  p += align256(sizeof(unsigned long long));
+  w.hist = (long long*)p;
+  p += align256(8 * 256 * sizeof(long long));
+  const int64_t M = (N_local > keep ? N_local : keep) + 1;
+  w.a = p;
+  w.b = p + align256((size_t)M * dsel_elem_bytes(dtype));
+  return w;
+}
+
+extern "C" int cacto_dselect_begin(int32_t dtype, int64_t N_local, int64_t keep, int64_t keep_global, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  if (keep < 0 || keep_global < 0 || N_local < 0 || !workspace)
+    return set_error(CACTO_EVALUE, "dselect: bad arguments");
+  if (workspace_bytes < cacto_dselect_workspace_bytes(dtype, N_local, keep))
+    return set_error(CACTO_EVALUE, "dselect: workspace too small");
+  DselWs w = dsel_ws(workspace, dtype, N_local, keep);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(workspace, 0, (char*)w.a - (char*)workspace, st) != cudaSuccess)
+    return set_error(CACTO_ECUDA, "dselect: memset failed");
+  DSelState s0{0ull, 0ull, (long long)keep_global, 0ll, 0ll};
+  if (cudaMemcpyAsync(w.st, &s0, sizeof(s0), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return set_error(CACTO_ECUDA, "dselect: state upload failed");
+  return CACTO_OK;
+}
+
+extern "C" int cacto_dselect_pass(int32_t dtype, const void* scores, int64_t N_local, int64_t keep, int32_t pass,
+                                  void* workspace, int64_t* hist_out, void* stream) {
+  const int KB = dtype == CACTO_F32 ? 32 : 64;
+  if (pass < 0 || pass >= KB / 8 || !hist_out) return set_error(CACTO_EVALUE, "dselect: bad pass %d", pass);
+  DselWs w = dsel_ws(workspace, dtype, N_local, keep);
+  cudaStream_t st = (cudaStream_t)stream;
+  long long* h = w.hist + pass * 256;
+  if (N_local > 0) {
+    int64_t blocks = (N_local + 255) / 256;
+    int64_t cap = 4 * (int64_t)num_sms();
+    if (blocks > cap) blocks = cap;
+    const int shift = KB - 8 * (pass + 1);
+    if (dtype == CACTO_F32)
+      dsel_hist_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)scores, N_local, shift, w.st, h);
+    else
+      dsel_hist_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double*)scores, N_local, shift, w.st, h);
+  }
+  if (cudaMemcpyAsync(hist_out, h, 256 * sizeof(long long), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return set_error(CACTO_ECUDA, "dselect: hist copy failed");
+  return check_launch("dsel_hist_kernel");
+}
+
+extern "C" int cacto_dselect_digit(int32_t dtype, int64_t N_local, int64_t keep, int32_t pass,
+                                   const int64_t* hist_global, void* workspace, int64_t* counts, void* stream) {
+  const int KB = dtype == CACTO_F32 ? 32 : 64;
+  if (pass < 0 || pass >= KB / 8 || !hist_global || !counts) return set_error(CACTO_EVALUE, "dselect: bad digit");
+  DselWs w = dsel_ws(workspace, dtype, N_local, keep);
+  dsel_digit_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(w.hist + pass * 256, (const long long*)hist_global,
+                                                          KB - 8 * (pass + 1), pass == KB / 8 - 1, w.st,
+                                                          (long long*)counts);
+  return check_launch("dsel_digit_kernel");
+}
+
+template <typename T, typename E>
+static int dsel_local(const T* scores, int64_t N, int64_t keep, int64_t base, int64_t n_cand, int64_t c, int64_t off,
+                      DselWs w, void* global, int64_t* local_sel, cudaStream_t st) {
+  if (n_cand > 0) {
+    int64_t blocks = (N + 255) / 256;
+    int64_t cap = 4 * (int64_t)num_sms();
+    if (blocks > cap) blocks = cap;
+    dsel_compact_kernel<T, E><<<(unsigned)blocks, 256, 0, st>>>(scores, N, base, w.st, (E*)w.a, w.cursor);
+  }
+  E* res = n_cand > 0 ? sort_pairs<E>((E*)w.a, (E*)w.b, n_cand, 0, st) : (E*)w.a;
+  if (c > 0) {
+    int64_t eb = (c + 255) / 256;
+    dsel_emit_local_kernel<E><<<(unsigned)(eb > 4096 ? 4096 : eb), 256, 0, st>>>(res, c, base, off, (E*)global,
+                                                                                local_sel);
+  }
+  return check_launch("dselect_local");
+}
+
+extern "C" int cacto_dselect_local(int32_t dtype, const void* scores, int64_t N_local, int64_t keep,
+                                   int64_t base_index, int64_t n_candidates, int64_t n_take, int64_t offset,
+                                   void* workspace, void* global_elems, int64_t* local_sel, void* stream) {
+  if (n_candidates < n_take || n_take < 0 || n_candidates > N_local || n_take > keep)
+    return set_error(CACTO_EVALUE, "dselect_local: bad counts");
+  if (dtype == CACTO_F32 && base_index + N_local > 0xFFFFFFFFll)
+    return set_error(CACTO_EVALUE, "dselect_local: global index exceeds 32 bits");
+  DselWs w = dsel_ws(workspace, dtype, N_local, keep);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CACTO_F32)
+    return dsel_local<float, Packed>((const float*)scores, N_local, keep, base_index, n_candidates, n_take, offset, w,
+                                     global_elems, local_sel, st);
+  return dsel_local<double, Pair>((const double*)scores, N_local, keep, base_index, n_candidates, n_take, offset, w,
+                                  global_elems, local_sel, st);
+}
+
+extern "C" int cacto_dselect_finish(int32_t dtype, void* global_elems, int64_t keep_global, int64_t* order,
+                                    void* top_scores, void* scratch, size_t scratch_bytes, void* stream) {
+  if (keep_global <= 0) return CACTO_OK;
+  const size_t eb = dsel_elem_bytes(dtype);
+  if (!global_elems || !order || !scratch || scratch_bytes < (size_t)keep_global * eb)
+    return set_error(CACTO_EVALUE, "dselect_finish: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t blocks = (keep_global + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (dtype == CACTO_F32) {
+    Packed* res = sort_pairs<Packed>((Packed*)global_elems, (Packed*)scratch, keep_global, 0, st);
+    emit_kernel<float, Packed><<<(unsigned)blocks, 256, 0, st>>>(res, keep_global, 0, order, (float*)top_scores);
+  } else {
+    Pair* res = sort_pairs<Pair>((Pair*)global_elems, (Pair*)scratch, keep_global, 0, st);
+    emit_kernel<double, Pair><<<(unsigned)blocks, 256, 0, st>>>(res, keep_global, 0, order, (double*)top_scores);
+  }
+  return check_launch("dselect_finish");
 }

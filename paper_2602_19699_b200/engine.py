@@ -11,6 +11,16 @@ graphs -- one critic+actor cycle (9 kernels) and one std cycle (4 kernels) --
 M times each.  Every per-cycle quantity (index list, Adam step, loss slot) is
 read from device counters, so the graphs are captured once and reused for
 every iteration.
+
+Data parallel (`dp_group`): every rank draws the same global index lists from
+the same generator (the reference stream), takes its contiguous slice
+[lo, hi) of each list (`parallel.shard_range`), and its losses divide by the
+GLOBAL minibatch (the actor's by the global live-row count, counted over the
+whole list), so the sum over ranks of the local gradients is the reference
+gradient.  Each update folds its partials into one [P + 1] vector (gradient +
+loss), sums it over ranks with one all-reduce, and applies the replicated
+fused Adam (+ Polyak) -- critic, then the actor on the UPDATED critic, then
+std, the dependency order of trainer.py:211-233.
 """
 
 from __future__ import annotations
@@ -21,7 +31,7 @@ from typing import Optional
 import numpy as np
 import torch
 
-from . import _lib, specs
+from . import _lib, parallel, specs
 from .buffer import ReplayBuffer
 from .device import DeviceNet, abi_dtype, device, torch_dtype
 
@@ -55,7 +65,7 @@ class UpdateEngine:
                  minibatch: int, k_s: float = 1.0, bootstrap: bool = True, tau: float = 0.005,
                  lr_actor: float = 5e-4, lr_critic: float = 1e-3, lr_std: float = 1e-3,
                  adam_states=None, precision: Optional[str] = None, use_graphs: bool = True,
-                 max_steps: int = 1 << 17):
+                 max_steps: int = 1 << 17, dp_group=None):
         self.model, self.field = model, field
         self.precision = precision or buffer.precision
         self.buffer = buffer
@@ -70,22 +80,36 @@ class UpdateEngine:
         self.costd = specs.cost_struct(model, field)
         dev = device()
         L = _lib.load()
-        B = self.B
+        # data parallel: this rank's slice [lo, hi) of every global minibatch
+        self.dp_group = dp_group
+        self.world, self.rank = 1, 0
+        if dp_group is not None:
+            import torch.distributed as dist
+            grp = None if dp_group == "world" else dp_group
+            self.dp_group = grp
+            self.world, self.rank = dist.get_world_size(grp), dist.get_rank(grp)
+        self.lo, self.hi = parallel.shard_range(self.B, self.rank, self.world)
+        if self.hi <= self.lo:
+            raise ValueError(f"minibatch {self.B} too small for {self.world} data-parallel ranks")
+        B = self.hi - self.lo
         self.ws_c = torch.empty(L.cacto_loss_workspace_bytes(self.critic.dn.desc, B), device=dev, dtype=torch.uint8)
         self.ws_a = torch.empty(L.cacto_loss_workspace_bytes(self.actor.dn.desc, B)
                                 + L.cacto_loss_workspace_bytes(self.critic.dn.desc, B), device=dev, dtype=torch.uint8)
         self.ws_s = torch.empty(L.cacto_loss_workspace_bytes(self.std.dn.desc, B), device=dev, dtype=torch.uint8)
         self.live = torch.zeros(1, device=dev, dtype=torch.int64)
+        if self.world > 1:  # folded gradient + loss of each net, the all-reduced vectors
+            dt = torch_dtype(self.precision)
+            self.g = {id(n): torch.zeros(n.dn.count + 1, device=dev, dtype=dt)
+                      for n in (self.actor, self.critic, self.std)}
+            import torch.distributed as dist
+            if use_graphs and dist.get_backend(self.dp_group) != "nccl":
+                use_graphs = False  # only NCCL collectives can be captured in a CUDA graph
         self.cnt = torch.zeros(2, device=dev, dtype=torch.int64)   # [critic/actor cycle, std cycle]
-        # bias-correction tables bc[t] = 1 - beta**t in Python double precision (nets.py:380-381)
-        t = np.arange(max_steps + 2, dtype=np.float64)
+        # bias-correction tables bc[t] = 1 - beta**t in Python double precision
+        # (nets.py:380-381), grown on demand (_ensure_bc) so any run length works
         self.bc = {}
-        for net in (self.actor, self.critic, self.std):
-            key = (net.beta1, net.beta2)
-            if key not in self.bc:
-                self.bc[key] = (torch.as_tensor(np.array([1.0 - net.beta1 ** k for k in t])).to(dev),
-                                torch.as_tensor(np.array([1.0 - net.beta2 ** k for k in t])).to(dev))
-        self.max_steps = max_steps
+        self.max_steps = 0
+        self._ensure_bc(max(int(max_steps), 1 + max(n.step for n in (self.actor, self.critic, self.std))))
         self.use_graphs = use_graphs
         self._graphs = None
         self._cap_M = 0
@@ -94,16 +118,46 @@ class UpdateEngine:
         self.sloss = None
         self.aloss = None
 
+    def _ensure_bc(self, need: int):
+        """Make the device tables cover Adam steps t <= need + 1 (doubling), so a
+        restored or long run never hits a fixed cap; growing them re-captures the
+        graphs (the table pointers are baked into the captured launches)."""
+        if need + 2 <= self.max_steps:
+            return
+        cap = max(1 << 17, self.max_steps)
+        while cap < need + 2:
+            cap *= 2
+        t = np.arange(cap, dtype=np.float64)
+        dev = device()
+        self.bc = {}
+        for net in (self.actor, self.critic, self.std):
+            key = (net.beta1, net.beta2)
+            if key not in self.bc:
+                self.bc[key] = (torch.as_tensor(np.array([1.0 - net.beta1 ** k for k in t])).to(dev),
+                                torch.as_tensor(np.array([1.0 - net.beta2 ** k for k in t])).to(dev))
+        self.max_steps = cap
+        self._graphs = None
+
     # -- one cycle, as kernel launches on the current stream -----------------------
-    def _batch(self, slot):
-        d = self.buffer.ring_desc(self.idx[slot], rows=self.B)
+    def _batch(self, slot, whole=False):
+        """Batch descriptor of cycle `cnt[slot]`: this rank's slice of the global
+        list (or the whole list), losses averaged over the global minibatch."""
+        lo, hi = (0, self.B) if whole else (self.lo, self.hi)
+        d = self.buffer.ring_desc(self.idx[slot, :, lo:], rows=hi - lo)
         d.cycle = self.cnt[slot:slot + 1].data_ptr()
         d.idx_stride = self.B
-        d.denom = 0
+        d.denom = self.B if self.world > 1 else 0
         return d
 
     def _adam(self, net: _Net, ws, npart, slot, target=None, loss=None):
         bc1, bc2 = self.bc[(net.beta1, net.beta2)]
+        if self.world > 1:
+            # fold -> [grad | loss] -> sum over ranks -> replicated Adam (+ Polyak)
+            g = self.g[id(net)]
+            _lib.call("cacto_reduce_grads", net.dn.desc.dtype, ws.data_ptr(), npart, net.dn.count, g.data_ptr(),
+                      g[net.dn.count:].data_ptr(), _stream())
+            parallel.allreduce_grads(g, self.dp_group)
+            ws, npart = g, 1
         _lib.call("cacto_reduce_adam_graph", net.dn.desc.dtype, ws.data_ptr(), npart, net.dn.count,
                   net.dn.params.data_ptr(), net.m.data_ptr(), net.v.data_ptr(), self.cnt[slot:slot + 1].data_ptr(),
                   net.base.data_ptr(), bc1.data_ptr(), bc2.data_ptr(), net.lr, net.beta1, net.beta2, net.eps,
@@ -119,9 +173,14 @@ class UpdateEngine:
                   int(self.bootstrap), self.ws_c.data_ptr(), self.ws_c.numel(), npart, st)
         self._adam(self.critic, self.ws_c, npart.value, 0, target=self.target, loss=self.closs)  # trainer.py:216-220
         npa = ctypes.c_int32(0)
-        # live rows (nets.py:310-312) counted inside the actor-loss launch (live_rows = NULL)
+        # live rows (nets.py:310-312): counted inside the actor-loss launch (live_rows =
+        # NULL), or over the whole global list when the batch is split over ranks
+        live = None
+        if self.world > 1:
+            _lib.call("cacto_count_live", self._batch(0, whole=True), self.live.data_ptr(), st)
+            live = self.live.data_ptr()
         _lib.call("cacto_actor_loss", self.actor.dn.desc, self.critic.dn.desc, self.sysd, self.costd, bd,
-                  None, self.ws_a.data_ptr(), self.ws_a.numel(), npa, st)
+                  live, self.ws_a.data_ptr(), self.ws_a.numel(), npa, st)
         self._adam(self.actor, self.ws_a, npa.value, 0, loss=self.aloss)                        # trainer.py:223-225
         _lib.call("cacto_counter_tick", self.cnt[0:1].data_ptr(), st)
 
@@ -178,8 +237,7 @@ class UpdateEngine:
             raise ValueError("m_updates must be >= 1")
         if self._cap_M < M:
             self._alloc(M)
-        if self.critic.step + M >= self.max_steps:
-            raise ValueError("Adam step table exhausted; raise max_steps")
+        self._ensure_bc(max(n.step for n in (self.actor, self.critic, self.std)) + M)
         # the reference's minibatch stream: M lists for critic/actor, then M for std
         lists = np.stack([self.buffer.draw_indices(self.B, rng) for _ in range(2 * M)])
         stage = torch.zeros((2, self._cap_M, self.B), dtype=torch.int64)

@@ -364,13 +364,11 @@ def actor_rollout_batch(actor, model, x0, t0=0, t_hor: Optional[int] = None, fie
     t0d = None if uniform else torch.as_tensor(t0a.astype(np.int32)).to(dev)
     t0s = int(t0a[0]) if N else 0
     _lib.call("cacto_rollout", sysd, costd, net.desc, x0d.data_ptr(),
-              t0d.data_ptr() if t0d is not None else None, t0s, N, T if t_hor is not None else 0,
+              t0d.data_ptr() if t0d is not None else None, t0s, N, T if t_hor is not None else _lib.FULL_HORIZON,
               *(out[k].data_ptr() if k in out else None for k in ("U", "X", "step_costs", "cost")),
               _stream())
     if as_numpy:
         out = {k: v.to("cpu", torch.float64).numpy() for k, v in out.items()}
-        if t_hor is None and "U" in out:
-            pass
     return out
 
 

@@ -1,18 +1,26 @@
 """Multi-GPU plumbing (one process per GPU, torch.distributed over NCCL).
 
 Rollouts and scoring shard by candidate index (contiguous ranges, no data-path
-collective); the only exchange is ONE all-gather of each shard's stable
-top-k winners (score, candidate index, start state), after which every rank
-merges identically (`cacto_select_merge`) and reproduces the single-device
-`np.argsort(-scores, kind="stable")[:keep]` exactly.
-Training is data parallel: the global minibatch index stream is identical on
-all ranks; rank r takes its slice and the flat gradient is all-reduced.
+collective).  The global stable top-k (`np.argsort(-scores, kind="stable")[:keep]`
+over the union of the shards, trainer.py:152) is found by a DISTRIBUTED radix
+threshold (`DistributedSelect`, csrc/select.cu `cacto_dselect_*`): per 8-bit
+digit one all-reduce of a 256-bin histogram (2 KB), then one all-gather of two
+counts per rank and one all-reduce of the keep_global winners (each rank fills
+its own disjoint segment of a zeroed buffer).  Traffic per rank is O(keep_global),
+not O(world * keep_global), and each rank keeps only its OWN winners' warm starts
+(no start states or controls cross ranks).
+Training is data parallel (engine.UpdateEngine(dp_group=...)): the global minibatch
+index stream is identical on all ranks; rank r takes its slice and the flat
+gradient is all-reduced.
+The older all-gather-and-merge path (`sharded_select`, `cacto_select_merge`) is
+kept as an independent check of the distributed select in the tests.
 """
 
 from __future__ import annotations
 
 from typing import Callable, Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -98,6 +106,108 @@ def sharded_select(local_scores: torch.Tensor, local_x0: torch.Tensor, base_inde
 
 def allreduce_grads(flat: torch.Tensor, group=None):
     """DP gradient sum over ranks (losses already divide by the GLOBAL batch)."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-    return flat
+    return all_reduce_sum(flat, group)
+
+
+# ---- collectives (gloo cannot reduce CUDA tensors on every build: stage via host) ----
+
+def _backend(group):
+    return dist.get_backend(group)
+
+
+def all_reduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place SUM over ranks (NCCL on device; gloo through a host copy)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return t
+    if t.is_cuda and _backend(group) != "nccl":
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def all_gather_cat(t: torch.Tensor, group=None) -> torch.Tensor:
+    """Concatenation over ranks (rank order) of equally shaped tensors."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return t.clone()
+    world = dist.get_world_size(group)
+    if t.is_cuda and _backend(group) != "nccl":
+        h = t.cpu()
+        parts = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(parts, h, group=group)
+        return torch.cat(parts).to(t.device)
+    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), device=t.device, dtype=t.dtype)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out
+
+
+class DistributedSelect:
+    """Exact global stable top-`keep_global` over contiguous candidate shards.
+
+    Every rank calls `run(local_scores, base_index)` with its shard (global
+    indices base_index .. base_index + N_local - 1, shards in rank order).
+    Returns (order [keep_global] global indices, scores [keep_global]) identical on
+    every rank, plus this rank's own winners: `local_sel` [c_r] (local indices,
+    in global order) -- the rows whose warm starts this rank hands to its TO.
+    Phases and collectives: see include/cacto_b200.h `cacto_dselect_*`.
+    """
+
+    def __init__(self, N_local: int, keep_global: int, dtype=torch.float32, group=None, device=None):
+        from . import _lib
+        self.L = _lib
+        self.group = group
+        self.N, self.keep = int(N_local), int(keep_global)
+        self.dtype = dtype
+        self.abi = _lib.F32 if dtype == torch.float32 else _lib.F64
+        self.passes = 4 if dtype == torch.float32 else 8
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.ws_bytes = _lib.load().cacto_dselect_workspace_bytes(self.abi, self.N, self.keep)
+        self.ws = torch.empty(self.ws_bytes, device=dev, dtype=torch.uint8)
+        self.hist = torch.empty(256, device=dev, dtype=torch.int64)
+        self.counts = torch.zeros(3, device=dev, dtype=torch.int64)
+        self.words = 1 if dtype == torch.float32 else 2
+        self.elems = torch.empty((max(self.keep, 1), self.words), device=dev, dtype=torch.int64)
+        self.scratch = torch.empty_like(self.elems)
+        self.order = torch.empty(self.keep, device=dev, dtype=torch.int64)
+        self.top = torch.empty(self.keep, device=dev, dtype=dtype)
+        self.local_sel = torch.empty(max(self.keep, 1), device=dev, dtype=torch.int64)
+        self.collectives = 0
+
+    def run(self, scores: torch.Tensor, base_index: int):
+        L, st = self.L, torch.cuda.current_stream().cuda_stream
+        if scores.shape[0] != self.N or scores.dtype != self.dtype:
+            raise ValueError("DistributedSelect: scores do not match the shard size / dtype")
+        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        rank = dist.get_rank(self.group) if dist.is_initialized() else 0
+        if self.keep > 0:
+            L.call("cacto_dselect_begin", self.abi, self.N, self.keep, self.keep, self.ws.data_ptr(), self.ws_bytes, st)
+            for p in range(self.passes):
+                L.call("cacto_dselect_pass", self.abi, scores.data_ptr(), self.N, self.keep, p, self.ws.data_ptr(),
+                       self.hist.data_ptr(), st)
+                all_reduce_sum(self.hist, self.group)
+                L.call("cacto_dselect_digit", self.abi, self.N, self.keep, p, self.hist.data_ptr(),
+                       self.ws.data_ptr(), self.counts.data_ptr(), st)
+            allc = all_gather_cat(self.counts[:2].contiguous(), self.group).view(world, 2).cpu().numpy()
+            need = int(self.counts[2].item())
+            self.collectives = self.passes + 2
+        else:
+            allc, need = np.zeros((world, 2), dtype=np.int64), 0
+        lt, eq = allc[:, 0], allc[:, 1]
+        before = np.concatenate([[0], np.cumsum(eq)[:-1]])
+        take = np.clip(need - before, 0, eq)
+        c = lt + take
+        if int(c.sum()) != self.keep:
+            raise RuntimeError(f"distributed select: {int(c.sum())} winners for keep={self.keep}")
+        off = int(c[:rank].sum())
+        cr = int(c[rank])
+        if self.keep > 0:
+            self.elems.zero_()
+            L.call("cacto_dselect_local", self.abi, scores.data_ptr(), self.N, self.keep, base_index,
+                   int(lt[rank] + eq[rank]), cr, off, self.ws.data_ptr(), self.elems.data_ptr(),
+                   self.local_sel.data_ptr(), st)
+            all_reduce_sum(self.elems, self.group)
+            L.call("cacto_dselect_finish", self.abi, self.elems.data_ptr(), self.keep, self.order.data_ptr(),
+                   self.top.data_ptr(), self.scratch.data_ptr(), self.scratch.numel() * 8, st)
+        return self.order, self.top, self.local_sel[:cr], off

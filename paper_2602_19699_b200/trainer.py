@@ -150,13 +150,12 @@ class BicPipeline:
         _lib.check(rc, "cacto_rollout_score")
         return scores, cost
 
-    def run(self, x0: torch.Tensor, keep: int, t0: int = 0, warm_starts: bool = True):
-        """x0 float64 [N, n] on device -> dict(order, scores, U, cost)."""
+    def _scores(self, x0: torch.Tensor, t0: int, reuse: bool):
+        """(scores [N], cost [N] or None, launches): K1 + K2 fused when possible."""
         N, n = x0.shape
         dt = torch_dtype(self.precision)
         launches = 0
         cost = None
-        reuse = warm_starts and keep > 0 and self.mode != "std"
         scores = None
         if self.mode != "std":
             scores, cost = self._fused(x0, t0, reuse)
@@ -169,6 +168,32 @@ class BicPipeline:
             xa[:, n] = float(t0)
             launches += 3  # torch copy + fill of the augmented view, K2 score
             scores = score_device(self.mode, xa, self.std, self.critic, cost)
+        return scores, cost, launches
+
+    def _warm(self, x0: torch.Tensor, sel: torch.Tensor, t0: int, reuse: bool):
+        """Warm starts U [K, T, m] of the candidates `sel` (local indices)."""
+        N = x0.shape[0]
+        K = sel.shape[0]
+        T = self.model.t_max - t0
+        U = torch.empty((K, T, self.model.m), device=x0.device, dtype=torch_dtype(self.precision))
+        if K == 0:
+            return U, 0
+        if reuse:
+            # the kept starts' controls from the cost rollout (same actor, start and t0:
+            # the trajectories trainer.py:192-193 would roll out again)
+            _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
+                      N, sel.data_ptr(), K, U.data_ptr(), _stream())
+            return U, 1
+        kept = x0.index_select(0, sel)
+        _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, K, T,
+                  U.data_ptr(), None, None, None, _stream())
+        return U, 2
+
+    def run(self, x0: torch.Tensor, keep: int, t0: int = 0, warm_starts: bool = True):
+        """x0 float64 [N, n] on device -> dict(order, scores, U, cost)."""
+        N, n = x0.shape
+        reuse = warm_starts and keep > 0 and self.mode != "std"
+        scores, cost, launches = self._scores(x0, t0, reuse)
         order, top = select_topk_device(scores, keep, 0, self.ws)
         if N <= 2048:
             launches += 1  # single-CTA select (csrc/select.cu small_select_kernel)
@@ -176,22 +201,37 @@ class BicPipeline:
             launches += 4 + max(0, int(np.ceil(np.log2(max(keep, 1) / 2048.0))))  # memset, select, sort, merges, emit
         out = {"order": order, "scores": top, "cost": cost}
         if warm_starts and keep > 0:
-            T = self.model.t_max - t0
-            U = torch.empty((keep, T, self.model.m), device=x0.device, dtype=dt)
-            if reuse:
-                # the kept starts' controls from the cost rollout (same actor, start and t0:
-                # the trajectories trainer.py:192-193 would roll out again)
-                _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
-                          N, order.data_ptr(), keep, U.data_ptr(), _stream())
-            else:
-                kept = x0.index_select(0, order)
-                launches += 1
-                _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, keep, T,
-                          U.data_ptr(), None, None, None, _stream())
-            launches += 1
-            out["U"] = U
+            out["U"], nl = self._warm(x0, order, t0, reuse)
+            launches += nl
         if self.base_index:
             out["order"] = order + self.base_index
+        self.kernel_launches = launches
+        return out
+
+    def run_sharded(self, x0: torch.Tensor, keep_global: int, base_index: int, dsel=None, group=None,
+                    t0: int = 0, warm_starts: bool = True):
+        """This rank's share of the multi-GPU rollout+BIC step.
+
+        x0 [N_local, n] are global candidates base_index .. base_index + N_local - 1
+        (contiguous shards in rank order).  Scores are local; the global stable
+        top-keep_global is found by the distributed radix threshold
+        (`parallel.DistributedSelect`).  Returns dict(order [keep_global] global
+        indices and scores, identical on every rank; local [c_r] this rank's own
+        winners as local indices in global order; U [c_r, T, m] their warm starts,
+        taken from this rank's cost rollout -- no states or controls cross ranks)."""
+        from .parallel import DistributedSelect
+        N = x0.shape[0]
+        reuse = warm_starts and keep_global > 0 and self.mode != "std"
+        scores, cost, launches = self._scores(x0, t0, reuse)
+        if dsel is None:
+            dsel = DistributedSelect(N, keep_global, scores.dtype, group, x0.device)
+        order, top, local, _ = dsel.run(scores, base_index)
+        # hist + digit per pass; compact, chunk sort, merges, emit; final chunk sort, merges, emit
+        launches += 2 * dsel.passes + 5 + 2 * max(0, int(np.ceil(np.log2(max(keep_global, 1) / 2048.0))))
+        out = {"order": order, "scores": top, "cost": cost, "local": local}
+        if warm_starts:
+            out["U"], nl = self._warm(x0, local, t0, reuse)
+            launches += nl
         self.kernel_launches = launches
         return out
 

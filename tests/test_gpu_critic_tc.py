@@ -3,7 +3,7 @@ tcgen05 layers with A in TMEM + batch-reduction GEMMs) against the float64
 oracle critic_loss (nets.py:233-290), which is pinned to the reference goldens.
 
 The path runs for fp32 3 x 64 critics at large batches; CACTO_CRITIC_TC_MIN=0
-forces it at test sizes.  Tolerances (fp32): loss 1e-4 rel, gradients 1e-3 of
+forces it at test sizes.  Tolerances (fp32): loss 1e-5 rel, gradients 1e-4 of
 max |grad| (the reference FD metric, test_nets.py:45-49).
 """
 
@@ -71,8 +71,8 @@ def test_critic_tc_vs_oracle(name, boot):
     b = batch(spec, 1000, rng)
     loss, grads = B_nets.critic_loss(critic, target, b, 0.7, boot)
     ref, ref_g = O_nets.critic_loss(critic, target, b, 0.7, boot)
-    assert loss == pytest.approx(ref, rel=1e-4)
-    grads_close(grads, ref_g, 1e-3)
+    assert loss == pytest.approx(ref, rel=1e-5)
+    grads_close(grads, ref_g, 1e-4)
 
 
 @pytest.mark.parametrize("R", [1, 127, 129, 20000])
@@ -83,8 +83,8 @@ def test_critic_tc_batch_sizes(R):
     b = batch(spec, R, rng)
     loss, grads = B_nets.critic_loss(critic, target, b, 1.0, True)
     ref, ref_g = O_nets.critic_loss(critic, target, b, 1.0, True)
-    assert loss == pytest.approx(ref, rel=1e-4)
-    grads_close(grads, ref_g, 1e-3)
+    assert loss == pytest.approx(ref, rel=1e-5)
+    grads_close(grads, ref_g, 1e-4)
 
 
 def test_critic_tc_tanh():
@@ -94,8 +94,8 @@ def test_critic_tc_tanh():
     b = batch(spec, 700, rng)
     loss, grads = B_nets.critic_loss(critic, target, b, 0.5, True)
     ref, ref_g = O_nets.critic_loss(critic, target, b, 0.5, True)
-    assert loss == pytest.approx(ref, rel=1e-4)
-    grads_close(grads, ref_g, 1e-3)
+    assert loss == pytest.approx(ref, rel=1e-5)
+    grads_close(grads, ref_g, 1e-4)
 
 
 def test_critic_tc_matches_simt_kernel():
@@ -109,5 +109,5 @@ def test_critic_tc_matches_simt_kernel():
         ls, gs = B_nets.critic_loss(critic, target, b, 1.0, True)
     finally:
         os.environ.pop("CACTO_CRITIC_TC", None)
-    assert lt == pytest.approx(ls, rel=1e-4)
-    grads_close(gt, gs, 1e-3)
+    assert lt == pytest.approx(ls, rel=1e-5)
+    grads_close(gt, gs, 1e-4)

@@ -1,0 +1,137 @@
+"""Edge cases of the drop-in boundary (advisor findings, round 1):
+
+  * `actor_rollout(..., t_hor=0)` from t0 < t_max returns the reference's 1-row
+    trajectory (nets.py:403-423) and writes nothing past its outputs -- the C ABI
+    uses CACTO_FULL_HORIZON (-1), not 0, for "every start to its own horizon";
+  * `cacto_select_merge` with several padded runs (keep > shard size) is exact
+    (the merge is stable for equal elements, so equal padding pairs of different
+    runs land in distinct slots);
+  * the UpdateEngine's Adam bias-correction tables grow on demand: a restored
+    Adam step beyond the initial 2^17 table runs, with the reference's
+    1 - beta**t values (nets.py:380-381).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2602_19699_b200 as P  # noqa: E402
+from paper_2602_19699_b200 import _lib, nets as B_nets, specs as B_specs, trainer as B_trainer  # noqa: E402
+from oracle import nets as O_nets, envs as O_envs  # noqa: E402
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("t0", [0, 37, 100])
+def test_rollout_t_hor_zero_is_one_row(prec, t0):
+    old = P.get_precision()
+    P.set_precision(prec)
+    try:
+        spec, fld = B_specs.config("dubins")
+        rng = np.random.default_rng(3)
+        c, h = B_specs.normalisation(spec)
+        actor = B_nets.init_mlp([6, 64, 64, 64, 2], rng, head="tanh", out_scale=spec.u_bound, in_center=c, in_half=h)
+        x0 = B_specs.TimeState(np.array([1.0, -2.0, 0.3, 0.1, -0.2]), t0)
+        tr = B_nets.actor_rollout(actor, spec, x0, 0, fld)
+        X, U, sc = O_nets.actor_rollout(actor, spec, x0.x, t0, 0, fld)
+        assert tr.X.shape == (1, 5) and tr.U.shape == (0, 2) and tr.step_costs.shape == (1,)
+        np.testing.assert_array_equal(tr.X, X.astype(np.float32) if prec == "fp32" else X)
+        np.testing.assert_allclose(tr.step_costs, sc, rtol=1e-6 if prec == "fp32" else 1e-12)
+        # batched, canaries around the outputs stay untouched
+        N = 300
+        xs = O_envs.sample_initial_states(spec, N, 5)
+        r = B_nets.actor_rollout_batch(actor, spec, xs, t0, 0, fld, as_numpy=False)
+        assert tuple(r["X"].shape) == (N, 1, 5) and tuple(r["step_costs"].shape) == (N, 1)
+        np.testing.assert_array_equal(r["X"][:, 0].cpu().double().numpy(),
+                                      torch.as_tensor(xs).to(r["X"].dtype).double().numpy())
+        _, _, scr, Jr = O_nets.actor_rollout_batch(actor, spec, xs, t0, 0, fld)
+        np.testing.assert_allclose(r["cost"].cpu().numpy(), Jr, rtol=1e-5 if prec == "fp32" else 1e-12)
+    finally:
+        P.set_precision(old)
+
+
+def test_rollout_t_hor_zero_does_not_write_past_outputs():
+    spec, fld = B_specs.config("pointmass")
+    actor = B_nets.init_mlp([5, 64, 64, 64, 2], np.random.default_rng(1), head="tanh", out_scale=spec.u_bound)
+    from paper_2602_19699_b200.device import device_net
+    dn = device_net(actor, "fp32")
+    N = 1000
+    x0 = torch.as_tensor(O_envs.sample_initial_states(spec, N, 2)).cuda()
+    arena = torch.full((4 * N * 8,), 7.0, device="cuda")   # X [N, 1, n] in the middle, canaries around
+    X = arena[N * 8:N * 8 + N * 4]
+    sc_arena = torch.full((3 * N,), 7.0, device="cuda")
+    SC = sc_arena[N:2 * N]
+    _lib.call("cacto_rollout", B_specs.system_struct(spec), B_specs.cost_struct(spec, fld), dn.desc, x0.data_ptr(),
+              None, 5, N, 0, None, X.data_ptr(), SC.data_ptr(), None, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.all(arena[:N * 8] == 7.0) and torch.all(arena[N * 8 + N * 4:] == 7.0)
+    assert torch.all(sc_arena[:N] == 7.0) and torch.all(sc_arena[2 * N:] == 7.0)
+    np.testing.assert_array_equal(X.view(N, 4).cpu().numpy(), x0.float().cpu().numpy())
+
+
+def test_rollout_rejects_bad_sentinels():
+    spec, fld = B_specs.config("pointmass")
+    actor = B_nets.init_mlp([5, 8, 2], np.random.default_rng(1), head="tanh", out_scale=spec.u_bound)
+    from paper_2602_19699_b200.device import device_net
+    dn = device_net(actor, "fp32")
+    x0 = torch.zeros((4, 4), device="cuda", dtype=torch.float64)
+    with pytest.raises(ValueError):
+        _lib.call("cacto_rollout", B_specs.system_struct(spec), None, dn.desc, x0.data_ptr(), None, 0, 4, -2,
+                  None, None, None, None, torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("R,shard,keep", [(4, 100, 300), (3, 1000, 2500), (5, 7, 30), (4, 5000, 4096)])
+def test_select_merge_padded_runs(dtype, R, shard, keep):
+    """Each shard's local top-min(keep, shard) padded to `keep` rows (parallel.gather_winners
+    layout: padding carries index -1), merged on device == the global stable argsort."""
+    rng = np.random.default_rng(R * shard + keep)
+    npdt, tdt = (np.float32, torch.float32) if dtype == "f32" else (np.float64, torch.float64)
+    N = R * shard
+    s = np.round(rng.normal(0, 1, N), 1).astype(npdt)
+    s[rng.integers(0, N, 3)] = np.nan
+    keep = min(keep, N)
+    rs = np.full(R * keep, np.nan, dtype=npdt)
+    ri = np.full(R * keep, -1, dtype=np.int64)
+    for r in range(R):
+        loc = s[r * shard:(r + 1) * shard]
+        k = min(keep, shard)
+        o = np.argsort(-loc, kind="stable")[:k]
+        rs[r * keep:r * keep + k] = loc[o]
+        ri[r * keep:r * keep + k] = r * keep + np.arange(k)          # positions (merge_positions)
+    M = R * keep
+    ws_bytes = 2 * (((M * 16) + 255) // 256) * 256
+    ws = torch.full((ws_bytes,), 0xAB, device="cuda", dtype=torch.uint8)   # stale workspace bytes
+    order = torch.empty(keep, device="cuda", dtype=torch.int64)
+    top = torch.empty(keep, device="cuda", dtype=tdt)
+    rs_d, ri_d = torch.as_tensor(rs).cuda(), torch.as_tensor(ri).cuda()   # alive across the launch
+    _lib.call("cacto_select_merge", _lib.F32 if dtype == "f32" else _lib.F64, rs_d.data_ptr(), ri_d.data_ptr(), R,
+              keep, order.data_ptr(), top.data_ptr(), ws.data_ptr(), ws_bytes, torch.cuda.current_stream().cuda_stream)
+    pos = order.cpu().numpy()
+    run, j = pos // keep, pos % keep
+    got = np.array([r * shard + np.argsort(-s[r * shard:(r + 1) * shard], kind="stable")[jj]
+                    for r, jj in zip(run, j)])
+    np.testing.assert_array_equal(got, np.argsort(-s, kind="stable")[:keep])
+
+
+def test_adam_tables_grow_past_initial_cap():
+    from dp_setup import engine_setup
+    old = P.get_precision()
+    P.set_precision("fp64")
+    try:
+        eng, seed = engine_setup(32)
+        start = (1 << 17) - 3
+        for n in (eng.actor, eng.critic, eng.std):
+            n.step = start
+        closs, _ = eng.run(6, np.random.default_rng(seed))
+        assert np.all(np.isfinite(closs))
+        assert eng.critic.step == start + 6 and eng.max_steps >= start + 8
+        bc1, bc2 = eng.bc[(0.9, 0.999)]
+        t = start + 6
+        assert bc1[t].item() == 1.0 - 0.9 ** float(t) and bc2[t].item() == 1.0 - 0.999 ** float(t)
+    finally:
+        P.set_precision(old)

@@ -2,13 +2,15 @@
 fixtures produced by the reference and against the CPU oracle.
 
 Tolerances (stated per test):
-  fp64 mode  rollouts 1e-9 rel (manipulator3 1e-6: chaotic amplification of the
+  fp64 mode  rollouts 1e-10 rel (manipulator3 1e-8: chaotic amplification of the
              closed-form 3x3 solve vs LAPACK), losses / grads 1e-10, Adam and
              Polyak bit-exact, select / gather / sampling bit-exact.
-  fp32 mode  rollout cost rel 2e-4 (pointmass, dubins, aliengo; 3000-start dubins
-             batch: median 1e-5 / p99 1e-4 / max 2e-3, chaotic tail); manipulator3
-             median 2e-3 / max 0.25 (chaotic tail, SURVEY.md D3); losses 1e-4 rel;
-             grads 1e-3 of max|grad| (the reference FD metric, test_nets.py:45-49).
+  fp32 mode  rollout cost rel 2e-5 (pointmass, dubins, aliengo; 3000-start dubins
+             batch: median 1e-6 / p99 1e-4 / max 2e-3, chaotic tail); manipulator3
+             median 1e-4 / max 0.1 (chaotic tail, SURVEY.md D3); losses 1e-6 rel;
+             grads 1e-5 of max|grad| (the reference FD metric, test_nets.py:45-49).
+  The SURVEY 8(c) contract itself, on the bench path at bench sizes, is
+  tests/test_gpu_contract.py.
 """
 
 import numpy as np
@@ -87,7 +89,7 @@ def test_batched_rollout_vs_reference(name, tag, precision):
     ref_cost = d[f"{key}_cost"]
     err = np.abs(r["cost"] - ref_cost) / np.maximum(1.0, np.abs(ref_cost))
     if precision == "fp64":
-        tol = 1e-6 if name == "manipulator3" else 1e-9
+        tol = 1e-8 if name == "manipulator3" else 1e-10
         assert err.max() < tol
         mask = ~np.isnan(d[f"{key}_X"])
         assert rel(r["X"][mask], d[f"{key}_X"][mask]) < tol
@@ -96,9 +98,9 @@ def test_batched_rollout_vs_reference(name, tag, precision):
         ms = ~np.isnan(d[f"{key}_step_costs"])
         np.testing.assert_array_equal(np.isnan(r["step_costs"]), ~ms)
     elif name == "manipulator3":
-        assert np.median(err) < 2e-3 and err.max() < 0.25
+        assert np.median(err) < 1e-4 and err.max() < 1e-1
     else:
-        assert err.max() < 2e-4
+        assert err.max() < 2e-5
 
 
 def test_single_rollout_dropin_and_no_field(fp64):
@@ -194,16 +196,16 @@ def test_critic_loss(key, boot, precision):
         assert loss == pytest.approx(ref, rel=1e-11)
         grads_close(grads, ref_g, 1e-10)
     else:
-        assert loss == pytest.approx(ref, rel=1e-4)
-        grads_close(grads, ref_g, 1e-3)
+        assert loss == pytest.approx(ref, rel=1e-6)
+        grads_close(grads, ref_g, 1e-5)
 
 
 def test_critic_loss_small_odd_shape(precision):
     d = G.load("losses")
     loss, grads = B_nets.critic_loss(net(d, "critic_small_net"), net(d, "critic_small_target"),
                                      G.batch(d, "critic_small"), 0.5, True)
-    assert loss == pytest.approx(float(d["critic_small_loss"]), rel=1e-11 if precision == "fp64" else 1e-4)
-    grads_close(grads, G.grads(d, "critic_small", 6), 1e-10 if precision == "fp64" else 1e-3)
+    assert loss == pytest.approx(float(d["critic_small_loss"]), rel=1e-11 if precision == "fp64" else 1e-6)
+    grads_close(grads, G.grads(d, "critic_small", 6), 1e-10 if precision == "fp64" else 1e-5)
 
 
 def test_critic_loss_perfect_critic_is_zero(fp64):
@@ -231,8 +233,8 @@ def test_critic_loss_rejects_empty_batch():
 def test_std_loss(key, precision):
     d = G.load("losses")
     loss, grads = B_nets.std_critic_loss(net(d, "std_net"), net(d, "critic_net"), G.batch(d, f"critic_{key}"))
-    assert loss == pytest.approx(float(d[f"std_{key}_loss"]), rel=1e-11 if precision == "fp64" else 1e-4)
-    grads_close(grads, G.grads(d, f"std_{key}", 8), 1e-10 if precision == "fp64" else 1e-3)
+    assert loss == pytest.approx(float(d[f"std_{key}_loss"]), rel=1e-11 if precision == "fp64" else 1e-6)
+    grads_close(grads, G.grads(d, f"std_{key}", 8), 1e-10 if precision == "fp64" else 1e-5)
 
 
 @pytest.mark.parametrize("name", ["pointmass", "dubins", "manipulator3", "aliengo_lipm"])
@@ -249,8 +251,8 @@ def test_actor_loss(name, precision):
         assert loss == pytest.approx(ref, rel=1e-10)
         grads_close(grads, G.grads(d, f"actor_{name}", 8), 1e-9)
     else:
-        assert loss == pytest.approx(ref, rel=1e-4, abs=1e-4)
-        grads_close(grads, G.grads(d, f"actor_{name}", 8), 2e-3)
+        assert loss == pytest.approx(ref, rel=1e-6)
+        grads_close(grads, G.grads(d, f"actor_{name}", 8), 1e-5)
 
 
 def test_actor_loss_all_at_horizon_raises():
