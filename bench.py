@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Benchmark: rollout+BIC states scored per second (BASELINE.json metric), on
-the configs[1] workload -- dubins (unicycle/car) reaching with obstacles,
-N = 65,536 candidate initial states per GPU, H = 64 networks, gap x std score.
+the largest single-GPU config -- configs[2], the 3-DoF planar manipulator
+reaching with obstacle avoidance, N = 262,144 candidate initial states per GPU,
+H = 64 networks, gap x std score.
 
 One step (metric 1) = for every candidate: a T-step
 actor rollout with running + terminal cost (K1), critic V(x0) and std sigma(x0)
@@ -12,13 +13,20 @@ states in pinned host memory and the kept indices + warm starts read back.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-Multi-GPU (torchrun): each rank scores its own 65,536-candidate shard (weak
-scaling), the shard winners are merged exactly with ONE NCCL all-gather, and
-each rank returns the warm starts of its slice of the global kept set.
+Multi-GPU (torchrun): each rank scores its own 262,144-candidate shard (weak
+scaling); the global stable top-k is found by a distributed radix threshold
+(4 all-reduces of a 2 KB histogram, one all-gather of 2 counts per rank, one
+all-reduce of the keep winners -- parallel.DistributedSelect), and each rank
+returns the warm starts of its OWN winners.
 
   --workload {dubins, pointmass, manipulator3, aliengo_lipm} selects the other
   BASELINE.json configs (N per GPU: 65,536 / 750 / 262,144 / 131,072 = the 1M
-AlienGO set sharded 8 ways); the default is configs[1] (dubins).
+AlienGO set sharded 8 ways); the default is manipulator3 (configs[2]).
+
+Reference arm (`--impl reference`): the UNMODIFIED reference `trajrl` from
+baseline/_ref (nets.actor_rollout per start on a process pool over all host
+cores, nets.mlp_forward scores, stable argsort, per-start warm-start rollouts --
+trainer.py:183-193), on a bounded sample of the same workload.
 """
 
 from __future__ import annotations
@@ -37,8 +45,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "rollout+BIC states scored/sec"
-CONFIG_NAME = "dubins"
-N_PER_GPU = 65536
+CONFIG_NAME = "manipulator3"
+N_PER_GPU = 262144
 WORKLOADS = {"dubins": 65536, "pointmass": 750, "manipulator3": 262144, "aliengo_lipm": 1 << 17}
 HIDDEN = 64
 CAND_MULT = 10
@@ -77,11 +85,23 @@ def candidates(spec, lo_row, count, seed=SEED):
 
 
 def flops_per_candidate(spec, T):
-    """GEMM FLOPs (2*MAC) per candidate: F_roll (1 + 1/cm) + 2 F_fwd."""
+    """GEMM FLOPs (2*MAC) per candidate actually executed: F_roll + 2 F_fwd.
+    (SURVEY 8d's total adds F_roll / cm for re-rolling the kept starts; here the
+    warm starts are the cost rollout's own controls, so that work is not done.)"""
     d, H, m = spec.n + 1, HIDDEN, spec.m
     f_roll = T * 2 * (d * H + 2 * H * H + H * m)
     f_fwd = 2 * (d * H + 2 * H * H + H)
-    return f_roll, f_roll * (1 + 1 / CAND_MULT) + 2 * f_fwd
+    return f_roll, f_roll + 2 * f_fwd
+
+
+def tensor_peak():
+    """Dense 16-bit tensor peak (the pipe K1's kind::f16 MMAs and the critic's run
+    on): MEASURED_PEAKS.json bf16 burst (kernels timed alone), else the fallback."""
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["bf16_tflops"]), "of measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS bf16 burst)"
+    except Exception:
+        return 1590.0, "of fallback (B200_PROFILING.md: 1.59 PFLOP/s bf16 burst)"
 
 
 # ---------------------------------------------------------------------------------
@@ -147,15 +167,29 @@ _W = {}
 
 
 def _worker_init(actor, spec, field):
+    """Pool worker: single-threaded BLAS; the reference objects built once
+    (the reference's own solve_batch pool pattern, ilqr.py:332-339)."""
     import threadpoolctl
     threadpoolctl.threadpool_limits(1)
-    _W.update(actor=actor, spec=spec, field=field)
+    _W.update(actor=actor, spec=spec, field=field, ref=None)
+    try:
+        from oracle import refarm
+        R = refarm.load()
+        _W["ref"] = (R, refarm.mlp(actor), refarm.model(spec), refarm.field(field))
+    except Exception as e:  # reference not installed: the oracle port
+        _W["ref_error"] = str(e)
 
 
 def _worker_rollouts(args):
-    from oracle import nets as O_nets
     x0s, with_field = args
     out = []
+    if _W.get("ref") is not None:
+        R, ra, rm, rf = _W["ref"]
+        for x0 in x0s:
+            tr = R.nets.actor_rollout(ra, rm, R.envs.TimeState(x0, 0), rm.t_max, rf if with_field else None)
+            out.append(float(tr.cost) if with_field else tr.U.shape[0])
+        return out
+    from oracle import nets as O_nets
     for x0 in x0s:
         X, U, sc = O_nets.actor_rollout(_W["actor"], _W["spec"], x0, 0, _W["spec"].t_max,
                                         _W["field"] if with_field else None)
@@ -163,32 +197,46 @@ def _worker_rollouts(args):
     return out
 
 
+def _worker_kind(_):
+    return "reference" if _W.get("ref") is not None else "port"
+
+
 def cpu_pipeline(spec, field, actor, critic, std, x0, pool, cores):
     """The reference hot path on the host, per candidate exactly as trajrl runs it:
     per-start actor_rollout with costs (nets.py:403-423), critic / std forward
     (nets.py:165-173), stable argsort select (trainer.py:150-153) and the
     per-start warm-start rollouts of the kept starts (trainer.py:192-193)."""
-    from oracle import nets as O_nets, select as O_select
     N = x0.shape[0]
     keep = max(1, N // CAND_MULT)
     chunks = [(x0[i::cores], True) for i in range(cores)]
     costs = np.empty(N)
     for i, res in enumerate(pool.map(_worker_rollouts, chunks)):
         costs[i::cores] = res
-    xa = O_select.augmented(x0)
-    s = O_select.std_scores(std, xa) * O_select.gap_scores(critic, xa, costs)
-    order = O_select.select_order(s, keep)
+    xa = np.concatenate([x0, np.zeros((N, 1))], axis=1)
+    try:
+        from oracle import refarm
+        R = refarm.load()
+        sig = R.nets.mlp_forward(refarm.mlp(std), xa)[:, 0]
+        V = R.nets.mlp_forward(refarm.mlp(critic), xa)[:, 0]
+    except Exception:
+        from oracle import nets as O_nets
+        sig = O_nets.mlp_forward(std, xa)[:, 0]
+        V = O_nets.mlp_forward(critic, xa)[:, 0]
+    s = sig * np.abs(V - costs)
+    order = np.argsort(-s, kind="stable")[:keep]
     kept = x0[order]
     list(pool.map(_worker_rollouts, [(kept[i::cores], False) for i in range(cores)]))
     return order
 
 
 def run_cpu(spec, field, actor, critic, std, sample, steps=1, warmup=0):
+    """(cores, per-step seconds, kind): kind "reference" when baseline/_ref loaded."""
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
     ctx = mp.get_context("fork")
     times = []
     with ctx.Pool(cores, initializer=_worker_init, initargs=(actor, spec, field)) as pool:
+        kind = "reference" if all(k == "reference" for k in pool.map(_worker_kind, range(cores))) else "port"
         x0 = candidates(spec, 0, sample)
         for i in range(warmup + steps):
             t0 = time.perf_counter()
@@ -196,7 +244,76 @@ def run_cpu(spec, field, actor, critic, std, sample, steps=1, warmup=0):
             dt = time.perf_counter() - t0
             if i >= warmup:
                 times.append(dt)
-    return cores, times
+    return cores, times, kind
+
+
+def critic_batch(spec, B, world=1, rank=0, seed=1):
+    """The synthetic replay rows and the global index stream of metric 2."""
+    from paper_2602_19699_b200 import specs
+    rng = np.random.default_rng(seed)
+    lo, hi = specs.region_box(spec)
+    rows = 1 << 18
+    xa = np.concatenate([rng.uniform(size=(rows, spec.n)) * (hi - lo) + lo,
+                         rng.integers(0, spec.t_max, (rows, 1))], axis=1)
+    xk = np.concatenate([rng.uniform(size=(rows, spec.n)) * (hi - lo) + lo,
+                         rng.integers(1, spec.t_max + 1, (rows, 1))], axis=1)
+    cols = (xa, rng.normal(size=(rows, spec.m)), rng.normal(size=rows), rng.normal(size=(rows, spec.n)), xk)
+    idx_all = rng.integers(0, rows, B * world)
+    return rows, cols, idx_all
+
+
+def cpu_critic_baseline(B=65536, reps=2):
+    """Metric 2 on the host: reference critic_loss (bootstrap on, k_s = 1) + adam_step
+    + polyak (nets.py:233-290, 375-398) on the same B-row batch, best of 1 thread and
+    all BLAS threads."""
+    import threadpoolctl
+    from paper_2602_19699_b200 import specs
+    spec, _ = specs.config("manipulator3")
+    _, critic, _ = make_nets(spec)
+    rows, cols, idx = critic_batch(spec, B)
+    kind = "reference"
+    try:
+        from oracle import refarm
+        R = refarm.load()
+        net, tgt = refarm.mlp(critic), refarm.mlp(critic)
+        batch = R.buffer.SampleBatch(*(c[idx] for c in cols), t_max=spec.t_max)
+        loss_fn, adam, polyak = R.nets.critic_loss, R.nets.adam_step, R.nets.polyak
+        state = R.nets.AdamState.init(net.flat_params())
+
+        def one():
+            nonlocal net, tgt, state
+            _, g = loss_fn(net, tgt, batch, 1.0, True)
+            p, state = adam(net.flat_params(), state, g)
+            net = net.with_params(p)
+            tgt = polyak(tgt, net, 0.005)
+    except Exception:
+        from types import SimpleNamespace
+        from oracle import nets as O_nets
+        kind = "port"
+        batch = SimpleNamespace(xa=cols[0][idx], u=cols[1][idx], v_bar=cols[2][idx], v_bar_x=cols[3][idx],
+                                xa_plus_k=cols[4][idx], t_max=spec.t_max)
+        p = list(critic.flat_params())
+        m = [np.zeros_like(x) for x in p]
+        v = [np.zeros_like(x) for x in p]
+
+        def one():
+            _, g = O_nets.critic_loss(critic, critic, batch, 1.0, True)
+            O_nets.adam_step(p, m, v, g, 0, 1e-3)
+    cores = len(os.sched_getaffinity(0))
+    best, best_threads = None, 1
+    for threads in sorted({1, cores}):
+        with threadpoolctl.threadpool_limits(threads):
+            one()  # warm-up
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                one()
+                dt = time.perf_counter() - t0
+                if best is None or dt < best:
+                    best, best_threads = dt, threads
+    return {"value": B / best, "unit": "samples/s", "cores": best_threads, "kind": kind,
+            "sample": f"one critic update at B={B}, H=64, manipulator3 dims: trajrl critic_loss + adam_step + "
+                      f"polyak, best of {reps} reps at 1 and {cores} BLAS threads (best: {best_threads}) "
+                      f"({cpu_model()})"}
 
 
 def cpu_model():
@@ -213,11 +330,8 @@ def cpu_model():
 # GPU arm
 # ---------------------------------------------------------------------------------
 
-TF32_DENSE_TFLOPS = 1100.0   # /opt/skills/guides/B200_PROFILING.md peak table (dense tf32)
-
-
 def measure_fp32_peak(torch, _lib, stream):
-    """FFMA throughput of this B200 (roofline denominator of the SIMT kernels)."""
+    """FFMA throughput of this B200 (the SIMT kernels' roofline, reported beside)."""
     blocks = 148 * 8
     iters = 4096
     out = torch.empty(blocks, device="cuda")
@@ -235,6 +349,43 @@ def measure_fp32_peak(torch, _lib, stream):
     return best
 
 
+def ncu_traffic(kernel_prefix, workload):
+    """dram bytes per launch of the kernel from the committed ncu --set full summary."""
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(prof.read_text())
+        e = d.get(f"{kernel_prefix}:{workload}")
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def reference_arm(args, spec, field, actor, critic, std, T, rank):
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    # bounded per-step sample: ~64 candidates per core (~0.8 s per step on manipulator3)
+    sample = min(args.cpu_sample or max(64, cores * 64), N_PER_GPU)
+    cores, times, kind = run_cpu(spec, field, actor, critic, std, sample, args.steps, max(1, args.warmup))
+    sec = float(np.mean(times))
+    val = sample / sec
+    what = ("trajrl (baseline/_ref, unmodified): nets.actor_rollout per start with the cost field, "
+            "nets.mlp_forward std/critic scores, np.argsort stable select, per-start warm-start rollouts"
+            if kind == "reference" else "oracle port of the reference path (baseline/_ref not importable)")
+    line = {"metric": METRIC, "value": val, "unit": "states/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (same starts and networks as the GPU arm)",
+            "impl": "reference",
+            "config": {"workload": f"{CONFIG_NAME} rollout+BIC, {sample} candidates per step (bounded CPU "
+                                   f"sample of the {N_PER_GPU}-candidate config), H={HIDDEN}, T={T}",
+                       "candidates_per_step": sample, "keep_fraction": 1 / CAND_MULT},
+            "cpu_baseline": {"value": val, "unit": "states/s", "cores": cores, "kind": kind,
+                             "sample": f"{sample} candidates/step on a {cores}-process pool ({cpu_model()}): "
+                                       + what},
+            "e2e": {"value": val, "unit": "states/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -242,7 +393,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cacto", choices=["cacto", "reference"])
     ap.add_argument("--n", type=int, default=0, help="candidates per GPU (0: the workload's)")
-    ap.add_argument("--workload", default="dubins", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="manipulator3", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="CPU baseline sample (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -265,26 +416,7 @@ def main():
     f_roll, f_cand = flops_per_candidate(spec, T)
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        cores = len(os.sched_getaffinity(0))
-        sample = min(args.cpu_sample or max(64, cores * 64), N_PER_GPU)    # ~0.6 s per step
-        cores, times = run_cpu(spec, field, actor, critic, std, sample, args.steps, max(1, args.warmup))
-        sec = float(np.mean(times))
-        val = sample / sec
-        line = {"metric": METRIC, "value": val, "unit": "states/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "impl": "reference",
-                "config": {"workload": f"{CONFIG_NAME} rollout+BIC, {sample} candidates per step (bounded CPU "
-                                       f"sample of the {N_PER_GPU}-candidate config), H={HIDDEN}, T={T}",
-                           "candidates_per_step": sample, "keep_fraction": 1 / CAND_MULT},
-                "cpu_baseline": {"value": val, "unit": "states/s", "cores": cores, "kind": "port",
-                                 "sample": f"{sample} candidates/step, per-start NumPy rollouts on a {cores}-process "
-                                           f"pool ({cpu_model()})"},
-                "e2e": {"value": val, "unit": "states/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
+        return reference_arm(args, spec, field, actor, critic, std, T, rank)
 
     import torch
     import torch.distributed as dist
@@ -303,23 +435,20 @@ def main():
     x0_pinned = torch.from_numpy(x0_host).pin_memory()
     x0_dev = x0_pinned.to("cuda")
     pipe = trainer.BicPipeline(spec, field, actor, critic, std, mode="std_x_gap", precision=args.precision)
+    dsel = None
+    if world > 1:
+        dsel = parallel.DistributedSelect(N, keep_global, torch.float32 if args.precision == "fp32" else torch.float64)
     flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")  # > 126 MB L2
 
     def step(x0):
         if world == 1:
             out = pipe.run(x0, keep_global)
             return out["order"], out["U"]
-        # every global winner is among its own shard's top-keep, so each rank keeps the
-        # warm starts of its local top-keep (taken from its cost rollout) and, after the
-        # exact merge, a mask of which of them made the global cut -- no second rollout
-        # and no control traffic between ranks
-        out = pipe.run(x0, min(keep_global, N), warm_starts=True)
-        rs, ro, rx = parallel.gather_winners(out["scores"], out["order"] + base,
-                                             x0.index_select(0, out["order"]), keep_global)
-        pos = parallel.merge_positions(rs, ro, keep_global, parallel.device_merge)
-        gorder = ro.index_select(0, pos)
-        kept = torch.isin(out["order"] + base, gorder)
-        return gorder, (out["U"], kept)
+        # shard-local K1+K2, the distributed exact select, and this rank's own
+        # winners' warm starts (taken from its cost rollout): no states or controls
+        # cross ranks, only the threshold histograms, counts and the keep winners
+        out = pipe.run_sharded(x0, keep_global, base, dsel=dsel)
+        return out["order"], out["U"]
 
     def timed(fn, K, W):
         for _ in range(W):
@@ -355,62 +484,51 @@ def main():
     launches_per_step = pipe.kernel_launches
 
     # ---- e2e through the public API: pinned host -> device -> kept order + U back --
-    keep_local_U = keep_global if world == 1 else min(keep_global, N)
     esz = 4 if args.precision == "fp32" else 8
     order_host = torch.empty(keep_global, dtype=torch.int64).pin_memory()
-    U_host = torch.empty((keep_local_U, T, spec.m), dtype=torch.float32 if esz == 4 else torch.float64).pin_memory()
-    mask_host = torch.empty(keep_local_U, dtype=torch.bool).pin_memory()
+    U_cap = keep_global if world == 1 else min(keep_global, N)
+    U_host = torch.empty((U_cap, T, spec.m), dtype=torch.float32 if esz == 4 else torch.float64).pin_memory()
+    d2h_rows = [0]
 
     def e2e_step():
         xd = x0_pinned.to("cuda", non_blocking=True)
         order, U = step(xd)
         order_host.copy_(order, non_blocking=True)
-        if world == 1:
-            U_host.copy_(U, non_blocking=True)
-        else:
-            U_host.copy_(U[0], non_blocking=True)
-            mask_host.copy_(U[1], non_blocking=True)
+        k = U.shape[0]
+        U_host[:k].copy_(U, non_blocking=True)
+        d2h_rows[0] = k
 
     e2e_ms = timed(e2e_step, args.steps, args.warmup)
     e2e_value = (N * world) / (e2e_ms * 1e-3)
     h2d = N * spec.n * 8
-    d2h = keep_global * 8 + keep_local_U * T * spec.m * esz + (keep_local_U if world > 1 else 0)
+    d2h = keep_global * 8 + d2h_rows[0] * T * spec.m * esz
 
-    # ---- roofline of the dominant kernel (K1 rollout over all candidates) ---------
-    x0r = x0_dev
+    # ---- roofline of the dominant kernel (the fused K1+K2 launch over all candidates) -
     for _ in range(2):
-        pipe.rollout_costs(x0r, keep_controls=True)
+        pipe._scores(x0_dev, 0, True)
     evs = []
     for _ in range(5):
+        flush.fill_(1.0)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        pipe.rollout_costs(x0r, keep_controls=True)
+        pipe._scores(x0_dev, 0, True)
         b.record()
         b.synchronize()
         evs.append(a.elapsed_time(b))
-    roll_ms = float(np.mean(evs))
-    achieved = f_roll * N / (roll_ms * 1e-3) / 1e12
+    k1_ms = float(np.mean(evs))
+    f_k1 = f_cand  # rollout + the std / critic forwards fused into the same launch
+    achieved = f_k1 * N / (k1_ms * 1e-3) / 1e12
     ffma_peak = measure_fp32_peak(torch, _lib, stream)
     tc_path = args.precision == "fp32" and os.environ.get("CACTO_ROLLOUT_TC", "1") != "0"
     if tc_path:
-        # K1 runs its policy layers on tcgen05 (kind::tf32, 3 MMA passes for fp32
-        # accuracy): the roofline is the TF32 tensor pipe
-        peak, bound = TF32_DENSE_TFLOPS, "tensor"
-        peak_source = ("B200_PROFILING.md fallback: tf32 dense 1.1 PFLOP/s, the fp32-class tensor format "
-                       "(MEASURED_PEAKS.json has no tf32 entry); algorithmic flops count each product once, the "
-                       "3xFP16 split issues 3x the MMAs at twice tf32's per-K rate")
-        kname = "rollout_tc_kernel (K1 on tcgen05, cost-only over all candidates)"
+        peak, peak_source = tensor_peak()
+        bound = "tensor"
+        kname = ("rollout_tc_kernel: K1 rollout with cost + K2 std/critic forwards in one tcgen05 launch "
+                 "(cacto_rollout_score), every candidate's controls kept for the warm starts")
     else:
         peak, bound = ffma_peak, "fp32_simt"
-        peak_source = "measured FFMA throughput on this GPU (cacto_fma_peak); MEASURED_PEAKS.json has no fp32 entry"
-        kname = "rollout_kernel (K1 SIMT, cost-only over all candidates)"
-    traffic = None
-    prof = ROOT / "profiles" / "rollout_ncu_summary.json"
-    if prof.exists() and args.workload == "dubins" and args.precision == "fp32":  # the captured launch
-        try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+        peak_source = "measured FFMA throughput on this GPU (cacto_fma_peak)"
+        kname = "rollout_kernel (K1 SIMT)"
 
     line = {
         "metric": METRIC, "value": value, "unit": "states/s", "n_gpus": world, "steps": args.steps,
@@ -418,21 +536,24 @@ def main():
         "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (uniform workspace starts, Glorot-init networks, actor output layer x10)",
         "config": {"workload": f"{CONFIG_NAME}: {N} candidate starts/GPU -> T={T} rollout with cost, "
-                               f"sigma*|V-J| score, stable top-{keep_global} select, kept warm starts (controls of the cost rollout)",
+                               f"sigma*|V-J| score, stable top-{keep_global} select, kept warm starts (controls of "
+                               f"the cost rollout)",
                    "candidates_per_gpu": N, "keep": keep_global, "hidden": [HIDDEN] * 3,
                    "horizon": T, "score": "std_x_gap", "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"shard-by-candidate x{world}"},
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "kernel": kname + ", emitting every candidate's controls (the kept warm starts)", "kernel_ms": roll_ms, "flops_per_candidate_rollout": f_roll,
+                     "frac": achieved / peak if peak else None,
+                     "traffic": ncu_traffic("rollout_tc_kernel", CONFIG_NAME) if tc_path else None,
+                     "kernel": kname, "kernel_ms": k1_ms,
+                     "flops_per_candidate": f_k1, "flops_rollout": f_roll,
                      "peak_source": peak_source,
                      "mma_passes": 3 if tc_path else None,
                      "mma_issued_tflops": 3 * achieved if tc_path else None,
-                     "mma_kind": "tcgen05 kind::f16, 3xFP16 split (fp16 dense peak 2250 TFLOP/s)" if tc_path else None,
-                     "binding_resource": ("CUDA-core epilogue issue (ncu: issue active ~71 %, tensor pipe ~25 %; "
-                                          "profiles/r01_ncu_rollout_tc.json)") if tc_path else None,
+                     "frac_of_3pass_ceiling": 3 * achieved / peak if tc_path else None,
+                     "mma_kind": "tcgen05 kind::f16, 3xFP16 split (each fp32 product = 3 fp16 MMAs)" if tc_path
+                     else None,
                      "fp32_ffma_peak": ffma_peak, "vs_ffma_peak": achieved / ffma_peak if ffma_peak else None},
         "clocks": clk,
         "flops_per_candidate": f_cand,
@@ -444,17 +565,20 @@ def main():
         try:
             line["secondary"] = critic_bench(torch, P, stream, world=world, rank=rank,
                                              dist=dist if world > 1 else None)
+            if rank == 0 and world == 1 and not args.no_cpu:
+                line["secondary"]["cpu_baseline"] = cpu_critic_baseline()
         except Exception as e:  # keep the primary line alive
             line["secondary"] = {"error": str(e)[:200]}
 
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
-        sample = min(args.cpu_sample or max(128, cores * 128), N)   # ~10 core-seconds of work
-        cores, times = run_cpu(spec, field, actor, critic, std, sample, 1, 1)
-        line["cpu_baseline"] = {"value": sample / times[0], "unit": "states/s", "cores": cores, "kind": "port",
+        sample = min(args.cpu_sample or max(128, cores * 128), N)   # ~10-20 core-seconds of work
+        cores, times, kind = run_cpu(spec, field, actor, critic, std, sample, 1, 1)
+        line["cpu_baseline"] = {"value": sample / times[0], "unit": "states/s", "cores": cores, "kind": kind,
                                 "sample": f"{sample} of the {N} candidates through the same pipeline: per-start "
-                                          f"NumPy rollouts on a {cores}-process pool ({cpu_model()})"}
+                                          f"trajrl actor_rollout on a {cores}-process pool ({cpu_model()})"
+                                          + ("" if kind == "reference" else " [oracle port]")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -479,16 +603,8 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
     tgt = DeviceNet(critic)
     cap = 1 << 20
     buf = ReplayBuffer(spec.n, spec.m, spec.t_max, capacity=cap)
-    rng = np.random.default_rng(1)
-    lo, hi = specs.region_box(spec)
-    rows = 1 << 18
-    xa = np.concatenate([rng.uniform(size=(rows, spec.n)) * (hi - lo) + lo,
-                         rng.integers(0, spec.t_max, (rows, 1))], axis=1)
-    xk = np.concatenate([rng.uniform(size=(rows, spec.n)) * (hi - lo) + lo,
-                         rng.integers(1, spec.t_max + 1, (rows, 1))], axis=1)
-    buf.push_many(SampleBatch(xa, rng.normal(size=(rows, spec.m)), rng.normal(size=rows),
-                              rng.normal(size=(rows, spec.n)), xk, spec.t_max))
-    idx_all = rng.integers(0, rows, B * world)           # the global stream, same on every rank
+    rows, cols, idx_all = critic_batch(spec, B, world, rank)   # the global stream, same on every rank
+    buf.push_many(SampleBatch(*cols, spec.t_max))
     idx = torch.as_tensor(idx_all[rank * B:(rank + 1) * B]).cuda()
     desc = buf.ring_desc(idx, rows=B)
     desc.denom = B * world                                 # mean over the global batch
@@ -535,10 +651,16 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
         ms = float(t.item())
     H, d = HIDDEN, spec.n + 1
     f = 28 * H * H + 14 * d * H + 8 * H
+    peak, peak_source = tensor_peak()
+    ach = f * B / (ms * 1e-3) / 1e12
     return {"metric": "critic Sobolev samples/sec", "value": B * world / (ms * 1e-3), "unit": "samples/s",
             "batch_per_gpu": B, "global_batch": B * world, "n_gpus": world, "hidden": [H] * 3,
             "ms_per_update": ms, "system": "manipulator3 (d=7)", "scaling": "weak",
-            "achieved_tflops": f * B * world / (ms * 1e-3) / 1e12, "flops_per_sample": f,
+            "achieved_tflops": ach, "flops_per_sample": f,
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                         "peak_source": peak_source,
+                         "kernel": "the whole update (critic_tc_kernel per-sample stage on tcgen05 + reduction "
+                                   "GEMMs + fold/Adam/Polyak), algorithmic F_critic = 28H^2+14dH+8H per sample"},
             "includes": "fused gather + target forward + Sobolev fwd/double-backprop + fold + "
                         + ("Adam + Polyak" if world == 1 else "NCCL all-reduce of the gradient + Adam + Polyak"),
             "sweep": "profiles/critic_sweep.py (batch 4k-1M x hidden 64-512, 1 GPU)"}

@@ -47,6 +47,32 @@ CACTO_D T softplus(T z) {
   if (z <= T(0)) return m_log1p(m_exp(z));
   return z;  // NaN
 }
+// fp32 cost-field terms on the SFU (the rollout epilogue's per-start work):
+// np.logaddexp(0, z) = max(z, 0) + log1p(exp(-|z|)) with ex2 / lg2.approx
+// (absolute error ~2e-7, vs the cost's O(10^2-10^3) per-step scale; log1p of a
+// small argument by its series), exp(x) = ex2(x log2 e).  NaN propagates,
+// +-inf give inf / 0 like NumPy.  fp64 keeps the libm forms (bit-level parity).
+CACTO_D float sfu_ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+CACTO_D float sfu_lg2(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+CACTO_D float cost_exp(float x) { return sfu_ex2(x * 1.4426950408889634f); }
+CACTO_D double cost_exp(double x) { return exp(x); }
+CACTO_D float cost_softplus(float z) {
+  const float e = sfu_ex2(-fabsf(z) * 1.4426950408889634f);
+  const float l = e < 1e-3f ? e * fmaf(-0.5f, e, 1.f) : sfu_lg2(1.f + e) * 0.6931471805599453f;
+  return fmaxf(z, 0.f) + l;
+}
+template <typename T>
+CACTO_D T softplus(T z);
+CACTO_D double cost_softplus(double z) { return softplus(z); }
+
 // exp(z - logaddexp(0, z)) (nets.py:59-60, costs.py:26-29)
 template <typename T>
 CACTO_D T sigmoid(T z) { return m_exp(z - softplus(z)); }

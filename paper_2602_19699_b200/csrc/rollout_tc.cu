@@ -323,7 +323,10 @@ static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   using PL = rtc::Plan<HP>;
   // 4 tiles: one epilogue warp per lane quadrant; fewer tiles: the columns are
   // split over more warps (shorter per-layer epilogue latency), 544 threads max
-  constexpr int SPLIT = NT == 4 ? 1 : (NT == 2 ? (HP >= 32 ? 2 : 1) : (HP >= 64 ? 4 : HP / 16));
+#ifndef CACTO_RTC_SPLIT4
+#define CACTO_RTC_SPLIT4 1
+#endif
+  constexpr int SPLIT = NT == 4 ? CACTO_RTC_SPLIT4 : (NT == 2 ? (HP >= 32 ? 2 : 1) : (HP >= 64 ? 4 : HP / 16));
   auto kern = a.act == CACTO_ACT_ELU ? rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_ELU>
                                      : rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_TANH>;
   constexpr uint32_t ACC = (uint32_t)(NT * SPLIT * 128 + 32) * 9 * 4;  // pairwise partial sums

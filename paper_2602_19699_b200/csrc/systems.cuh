@@ -285,11 +285,11 @@ CACTO_D T point_value(const CostDev<T>& C, T px, T py) {
   T rx = px - C.tx, ry = py - C.ty;
   T q = rx * rx + ry * ry;
   T val = C.w_d * q;
-  val -= C.w_r * m_exp(-q / C.rho2);
+  val -= C.w_r * cost_exp(-q / C.rho2);
   for (int i = 0; i < C.n_obs; ++i) {
     T dx = px - C.ocx[i], dy = py - C.ocy[i];
     T e = dx * (C.e00[i] * dx + C.e01[i] * dy) + dy * (C.e10[i] * dx + C.e11[i] * dy);
-    val += C.w_o * softplus(T(10) * (T(1) - e));
+    val += C.w_o * cost_softplus(T(10) * (T(1) - e));
   }
   return val;
 }
@@ -324,15 +324,15 @@ CACTO_D T terminal_cost(const SysDev<T>& P, const CostDev<T>& C, const T* x) {
     T cx = x[4], cy = x[5], vx = x[6], vy = x[7];
     T q = cx * cx + cy * cy, v2 = vx * vx + vy * vy;
     T val = C.w_d * q;
-    val -= C.w_r * m_exp(-q / C.rho2);
+    val -= C.w_r * cost_exp(-q / C.rho2);
     val += C.w_vel * v2;
-    val += C.w_vbar * softplus(T(10) * (v2 - C.v_max2));
+    val += C.w_vbar * cost_softplus(T(10) * (v2 - C.v_max2));
     T ox = cx - x[9], oy = cy - x[10];
-    val += C.w_o * softplus(T(10) * (T(1) - (ox * ox + oy * oy) / C.obs_r2));
-    val += C.w_wall * softplus(T(10) * (x[11] - cx));
-    val += C.w_wall * softplus(T(10) * (cx - x[12]));
-    val += C.w_wall * softplus(T(10) * (x[13] - cy));
-    val += C.w_wall * softplus(T(10) * (cy - x[14]));
+    val += C.w_o * cost_softplus(T(10) * (T(1) - (ox * ox + oy * oy) / C.obs_r2));
+    val += C.w_wall * cost_softplus(T(10) * (x[11] - cx));
+    val += C.w_wall * cost_softplus(T(10) * (cx - x[12]));
+    val += C.w_wall * cost_softplus(T(10) * (x[13] - cy));
+    val += C.w_wall * cost_softplus(T(10) * (cy - x[14]));
     return val;
   } else {
     T px, py;
