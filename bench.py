@@ -503,6 +503,23 @@ def main():
     h2d = N * spec.n * 8
     d2h = keep_global * 8 + d2h_rows[0] * T * spec.m * esz
 
+    # ---- e2e with the candidates generated on the device (the reference's seeded
+    #      sample_initial_states replayed bit-exactly, sampling.py): only the 32-byte
+    #      PCG64 state goes in; the kept order + warm starts come back ------------------
+    from paper_2602_19699_b200.sampling import sample_initial_states_device
+    x0_seeded = torch.empty_like(x0_dev)
+
+    def e2e_seeded_step():
+        sample_initial_states_device(spec, N * world, SEED, first_row=base, rows=N, out=x0_seeded)
+        order, U = step(x0_seeded)
+        order_host.copy_(order, non_blocking=True)
+        k = U.shape[0]
+        U_host[:k].copy_(U, non_blocking=True)
+
+    e2e_s_ms = timed(e2e_seeded_step, args.steps, args.warmup)
+    if not torch.equal(x0_seeded, x0_dev):
+        raise RuntimeError("device-sampled candidates differ from the host draw")
+
     # ---- roofline of the dominant kernel (the fused K1+K2 launch over all candidates) -
     for _ in range(2):
         pipe._scores(x0_dev, 0, True)
@@ -542,6 +559,10 @@ def main():
                    "horizon": T, "score": "std_x_gap", "l2": "flushed between timed steps (256 MB write)",
                    "parallelism": f"shard-by-candidate x{world}"},
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e_device_sampled": {"value": (N * world) / (e2e_s_ms * 1e-3), "unit": "states/s",
+                               "h2d_bytes_per_step": 32, "d2h_bytes_per_step": d2h,
+                               "note": "candidates = device PCG64 replay of sample_initial_states(seed) "
+                                       "(bit-identical to the host draw, checked), as run_iteration uses"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None,

@@ -88,9 +88,13 @@ def run_iteration(state, iter_idx: int, trajrl):
     else:
         n_sel = cfg.later_batch
         if cfg.bic:
-            cands = T.sample_initial_states(model, cfg.candidate_multiplier * n_sel,
-                                            T._seed_int(cfg.seed, 1, iter_idx), T.Region.WORKSPACE)
-            starts = B_trainer.select_initial_states_bic(cands, state.std, n_sel)
+            # candidates generated on the device (bit-exact PCG64 replay of
+            # sample_initial_states, envs/__init__.py:112-122), scored and selected
+            # there; only the kept starts come back (trainer.py:183-186)
+            kept, _ = B_trainer.sample_select_bic(model, cfg.candidate_multiplier * n_sel,
+                                                  T._seed_int(cfg.seed, 1, iter_idx), state.std, n_sel,
+                                                  T.Region.WORKSPACE)
+            starts = [T.TimeState(x=row, t=0) for row in kept]
         else:
             starts = T.sample_initial_states(model, n_sel, T._seed_int(cfg.seed, 1, iter_idx), T.Region.WORKSPACE)
         starts = T._assign_start_times(starts, model, cfg, iter_idx)

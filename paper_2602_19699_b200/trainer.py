@@ -80,6 +80,25 @@ def select_initial_states_bic(candidates, std_net, keep: int):
     return [candidates[i] for i in order.cpu().numpy()]
 
 
+def sample_select_bic(model, count: int, rng_seed, std_net, keep: int, region=specs.Region.WORKSPACE):
+    """`select_initial_states_bic(sample_initial_states(model, count, rng_seed, region),
+    std_net, keep)` (trainer.py:183-186) with the candidates generated, scored and
+    selected on the device: the count x n candidate block is the bit-exact device
+    replay of the reference's PCG64 stream (sampling.py), so only the kept rows
+    cross PCIe.  Returns (kept states [keep, n] float64 NumPy, kept candidate
+    indices) in the reference's order."""
+    from .sampling import sample_initial_states_device
+    if keep > count:
+        raise ValueError(f"keep={keep} exceeds {count} candidates")
+    x = sample_initial_states_device(model, count, rng_seed, region)
+    sn = device_net(std_net)
+    xa = torch.zeros((count, int(model.n) + 1), device=x.device, dtype=torch_dtype(sn.precision))
+    xa[:, :-1] = x
+    scores = score_device("std", xa, std_net=sn)
+    order, _ = select_topk_device(scores, keep)
+    return x.index_select(0, order).cpu().numpy(), order.cpu().numpy()
+
+
 class BicPipeline:
     """Rollout + BIC scoring + stable selection + warm starts, device resident.
 

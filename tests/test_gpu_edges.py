@@ -135,3 +135,25 @@ def test_adam_tables_grow_past_initial_cap():
         assert bc1[t].item() == 1.0 - 0.9 ** float(t) and bc2[t].item() == 1.0 - 0.999 ** float(t)
     finally:
         P.set_precision(old)
+
+
+@pytest.mark.parametrize("name,count,keep", [("pointmass", 750, 75), ("dubins", 65536, 6553),
+                                             ("manipulator3", 20000, 2000)])
+def test_device_sampled_bic_equals_host_sampled(name, count, keep):
+    """trainer.py:183-186 on the device: the PCG64 replay gives the reference's
+    candidates bit-exactly, so the kept starts (rows and order) equal the host
+    path's select_initial_states_bic(sample_initial_states(...)) on the same scores."""
+    from paper_2602_19699_b200 import specs
+    spec, _ = B_specs.config(name)
+    rng = np.random.default_rng(7)
+    c, h = B_specs.normalisation(spec)
+    std = B_nets.init_mlp([spec.n + 1, 64, 64, 64, 1], rng, head="std", in_center=c, in_half=h)
+    seed = O_envs.seed_int(3, 1, 5)
+    kept, order = B_trainer.sample_select_bic(spec, count, seed, std, keep)
+    cands = [specs.TimeState(x, 0) for x in O_envs.sample_initial_states(spec, count, seed)]
+    ref = B_trainer.select_initial_states_bic(cands, std, keep)
+    np.testing.assert_array_equal(kept, np.stack([s.x for s in ref]))
+    # and the device block itself is the host draw, bit for bit
+    from paper_2602_19699_b200.sampling import sample_initial_states_device
+    x = sample_initial_states_device(spec, count, seed, first_row=count // 3, rows=count // 2).cpu().numpy()
+    np.testing.assert_array_equal(x, O_envs.sample_initial_states(spec, count, seed)[count // 3:count // 3 + count // 2])
