@@ -143,6 +143,46 @@ def all_gather_cat(t: torch.Tensor, group=None) -> torch.Tensor:
     return out
 
 
+class _DselectKernels:
+    """The device phases of the distributed select (csrc/select.cu cacto_dselect_*)."""
+
+    def __init__(self, N_local, keep, dtype, device):
+        from . import _lib
+        self.L = _lib
+        self.N, self.keep, self.dtype = N_local, keep, dtype
+        self.abi = _lib.F32 if dtype == torch.float32 else _lib.F64
+        self.passes = 4 if dtype == torch.float32 else 8
+        self.words = 1 if dtype == torch.float32 else 2
+        self.device = device
+        self.ws_bytes = _lib.load().cacto_dselect_workspace_bytes(self.abi, self.N, self.keep)
+        self.ws = torch.empty(self.ws_bytes, device=device, dtype=torch.uint8)
+        self.scratch = torch.empty((max(keep, 1), self.words), device=device, dtype=torch.int64)
+
+    @staticmethod
+    def _st():
+        return torch.cuda.current_stream().cuda_stream
+
+    def begin(self):
+        self.L.call("cacto_dselect_begin", self.abi, self.N, self.keep, self.keep, self.ws.data_ptr(), self.ws_bytes,
+                    self._st())
+
+    def hist(self, scores, p, out):
+        self.L.call("cacto_dselect_pass", self.abi, scores.data_ptr(), self.N, self.keep, p, self.ws.data_ptr(),
+                    out.data_ptr(), self._st())
+
+    def digit(self, p, hist_global, counts):
+        self.L.call("cacto_dselect_digit", self.abi, self.N, self.keep, p, hist_global.data_ptr(), self.ws.data_ptr(),
+                    counts.data_ptr(), self._st())
+
+    def local(self, scores, base, n_cand, n_take, off, elems, local_sel):
+        self.L.call("cacto_dselect_local", self.abi, scores.data_ptr(), self.N, self.keep, base, n_cand, n_take, off,
+                    self.ws.data_ptr(), elems.data_ptr(), local_sel.data_ptr(), self._st())
+
+    def finish(self, elems, order, top):
+        self.L.call("cacto_dselect_finish", self.abi, elems.data_ptr(), self.keep, order.data_ptr(), top.data_ptr(),
+                    self.scratch.data_ptr(), self.scratch.numel() * 8, self._st())
+
+
 class DistributedSelect:
     """Exact global stable top-`keep_global` over contiguous candidate shards.
 
@@ -151,63 +191,61 @@ class DistributedSelect:
     Returns (order [keep_global] global indices, scores [keep_global]) identical on
     every rank, plus this rank's own winners: `local_sel` [c_r] (local indices,
     in global order) -- the rows whose warm starts this rank hands to its TO.
-    Phases and collectives: see include/cacto_b200.h `cacto_dselect_*`.
+    Phases and collectives: see include/cacto_b200.h `cacto_dselect_*`; the
+    host side here owns only the collectives and the tie split between ranks.
+    `kernels` (tests only) swaps the device phases for a stand-in.
     """
 
-    def __init__(self, N_local: int, keep_global: int, dtype=torch.float32, group=None, device=None):
-        from . import _lib
-        self.L = _lib
+    def __init__(self, N_local: int, keep_global: int, dtype=torch.float32, group=None, device=None, kernels=None):
         self.group = group
         self.N, self.keep = int(N_local), int(keep_global)
         self.dtype = dtype
-        self.abi = _lib.F32 if dtype == torch.float32 else _lib.F64
-        self.passes = 4 if dtype == torch.float32 else 8
-        dev = device or torch.device("cuda", torch.cuda.current_device())
-        self.ws_bytes = _lib.load().cacto_dselect_workspace_bytes(self.abi, self.N, self.keep)
-        self.ws = torch.empty(self.ws_bytes, device=dev, dtype=torch.uint8)
+        if kernels is None:
+            dev = device or torch.device("cuda", torch.cuda.current_device())
+            kernels = _DselectKernels(self.N, self.keep, dtype, dev)
+        self.k = kernels
+        self.passes = self.k.passes
+        dev = self.k.device
         self.hist = torch.empty(256, device=dev, dtype=torch.int64)
         self.counts = torch.zeros(3, device=dev, dtype=torch.int64)
-        self.words = 1 if dtype == torch.float32 else 2
-        self.elems = torch.empty((max(self.keep, 1), self.words), device=dev, dtype=torch.int64)
-        self.scratch = torch.empty_like(self.elems)
+        self.elems = torch.empty((max(self.keep, 1), self.k.words), device=dev, dtype=torch.int64)
         self.order = torch.empty(self.keep, device=dev, dtype=torch.int64)
         self.top = torch.empty(self.keep, device=dev, dtype=dtype)
         self.local_sel = torch.empty(max(self.keep, 1), device=dev, dtype=torch.int64)
         self.collectives = 0
 
+    @staticmethod
+    def split(lt, eq, need, rank, keep):
+        """Tie split between ranks (host): rank r takes its first
+        take_r = clamp(need - sum_{q<r} eq_q, 0, eq_r) keys equal to the threshold
+        (lower ranks hold lower global indices), so c_r = lt_r + take_r winners at
+        offset sum_{q<r} c_q of the concatenated winner buffer."""
+        lt, eq = np.asarray(lt, np.int64), np.asarray(eq, np.int64)
+        before = np.concatenate([[0], np.cumsum(eq)[:-1]])
+        take = np.clip(need - before, 0, eq)
+        c = lt + take
+        if int(c.sum()) != keep:
+            raise RuntimeError(f"distributed select: {int(c.sum())} winners for keep={keep}")
+        return int(c[:rank].sum()), int(c[rank])
+
     def run(self, scores: torch.Tensor, base_index: int):
-        L, st = self.L, torch.cuda.current_stream().cuda_stream
         if scores.shape[0] != self.N or scores.dtype != self.dtype:
             raise ValueError("DistributedSelect: scores do not match the shard size / dtype")
         world = dist.get_world_size(self.group) if dist.is_initialized() else 1
         rank = dist.get_rank(self.group) if dist.is_initialized() else 0
-        if self.keep > 0:
-            L.call("cacto_dselect_begin", self.abi, self.N, self.keep, self.keep, self.ws.data_ptr(), self.ws_bytes, st)
-            for p in range(self.passes):
-                L.call("cacto_dselect_pass", self.abi, scores.data_ptr(), self.N, self.keep, p, self.ws.data_ptr(),
-                       self.hist.data_ptr(), st)
-                all_reduce_sum(self.hist, self.group)
-                L.call("cacto_dselect_digit", self.abi, self.N, self.keep, p, self.hist.data_ptr(),
-                       self.ws.data_ptr(), self.counts.data_ptr(), st)
-            allc = all_gather_cat(self.counts[:2].contiguous(), self.group).view(world, 2).cpu().numpy()
-            need = int(self.counts[2].item())
-            self.collectives = self.passes + 2
-        else:
-            allc, need = np.zeros((world, 2), dtype=np.int64), 0
-        lt, eq = allc[:, 0], allc[:, 1]
-        before = np.concatenate([[0], np.cumsum(eq)[:-1]])
-        take = np.clip(need - before, 0, eq)
-        c = lt + take
-        if int(c.sum()) != self.keep:
-            raise RuntimeError(f"distributed select: {int(c.sum())} winners for keep={self.keep}")
-        off = int(c[:rank].sum())
-        cr = int(c[rank])
-        if self.keep > 0:
-            self.elems.zero_()
-            L.call("cacto_dselect_local", self.abi, scores.data_ptr(), self.N, self.keep, base_index,
-                   int(lt[rank] + eq[rank]), cr, off, self.ws.data_ptr(), self.elems.data_ptr(),
-                   self.local_sel.data_ptr(), st)
-            all_reduce_sum(self.elems, self.group)
-            L.call("cacto_dselect_finish", self.abi, self.elems.data_ptr(), self.keep, self.order.data_ptr(),
-                   self.top.data_ptr(), self.scratch.data_ptr(), self.scratch.numel() * 8, st)
+        if self.keep == 0:
+            return self.order, self.top, self.local_sel[:0], 0
+        self.k.begin()
+        for p in range(self.passes):
+            self.k.hist(scores, p, self.hist)
+            all_reduce_sum(self.hist, self.group)
+            self.k.digit(p, self.hist, self.counts)
+        allc = all_gather_cat(self.counts[:2].contiguous(), self.group).view(world, 2).cpu().numpy()
+        need = int(self.counts[2].item())
+        self.collectives = self.passes + 2
+        off, cr = self.split(allc[:, 0], allc[:, 1], need, rank, self.keep)
+        self.elems.zero_()
+        self.k.local(scores, base_index, int(allc[rank, 0] + allc[rank, 1]), cr, off, self.elems, self.local_sel)
+        all_reduce_sum(self.elems, self.group)
+        self.k.finish(self.elems, self.order, self.top)
         return self.order, self.top, self.local_sel[:cr], off

@@ -87,3 +87,45 @@ def test_shard_ranges_partition():
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             sizes = [h - l for l, h in rs]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _dsel_worker(rank, world, port, scores_all, keep, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from dselect_standin import NumpyDselect
+        N = scores_all.shape[0]
+        lo, hi = parallel.shard_range(N, rank, world)
+        ds = parallel.DistributedSelect(hi - lo, keep, torch.float32, kernels=NumpyDselect(hi - lo, keep))
+        order, _, local, off = ds.run(torch.as_tensor(scores_all[lo:hi]), lo)
+        out[rank] = (order.numpy().copy(), local.numpy().copy() + lo, ds.collectives)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("N,keep,kind", [(1000, 100, "ties"), (999, 37, "normal"), (64, 64, "ties"),
+                                         (4001, 400, "const"), (10, 1, "normal")])
+def test_distributed_select_host_logic(world, N, keep, kind):
+    """DistributedSelect's collectives and tie split (4 histogram all-reduces, one
+    all-gather of counts, one all-reduce of the winners) with the device phases
+    replaced by a NumPy stand-in: every rank gets the global stable argsort and
+    exactly its own winners."""
+    rng = np.random.default_rng(N + world)
+    s = {"ties": np.round(rng.normal(0, 1, N), 1), "normal": rng.normal(0, 1, N), "const": np.full(N, 2.0)}[kind]
+    s = s.astype(np.float32)
+    s[rng.integers(0, N, 3)] = np.nan
+    s[rng.integers(0, N, 3)] = -0.0
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_dsel_worker, args=(world, _free_port(), s, keep, out), nprocs=world, join=True,
+                       start_method="fork")
+    ref = np.argsort(-s, kind="stable")[:keep]
+    mine = []
+    for r in range(world):
+        order, local, ncoll = out[r]
+        np.testing.assert_array_equal(order, ref)
+        np.testing.assert_array_equal(local, ref[np.isin(ref, local)])
+        assert ncoll == 6
+        mine.append(local)
+    np.testing.assert_array_equal(np.sort(np.concatenate(mine)), np.sort(ref))
