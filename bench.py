@@ -588,8 +588,37 @@ def main():
                                              dist=dist if world > 1 else None)
             if rank == 0 and world == 1 and not args.no_cpu:
                 line["secondary"]["cpu_baseline"] = cpu_critic_baseline()
+            # the config-5 grid (batch 4k-1M x hidden 64-512), device-timed, this GPU count
+            grid = []
+            for Hs in (64, 128, 256, 512):
+                for Bs in (4096, 65536, 1 << 20):
+                    r = critic_bench(torch, P, stream, B=Bs, world=world, rank=rank,
+                                     dist=dist if world > 1 else None, H=Hs, K=3 if Bs >= (1 << 20) else 5)
+                    grid.append({"hidden": Hs, "batch_per_gpu": Bs, "samples_per_s": r["value"],
+                                 "ms_per_update": r["ms_per_update"], "tflops": r["achieved_tflops"],
+                                 "frac": r["roofline"]["frac"]})
+                    torch.cuda.empty_cache()
+            line["secondary"]["sweep"] = grid
         except Exception as e:  # keep the primary line alive
             line["secondary"] = {"error": str(e)[:200]}
+
+    # ---- per-iteration wall clock (north_star): the reference's
+    #      run_iteration vs the installed hot path on pointmass.ini, TO on the CPU in
+    #      both arms (bench_iteration.py) --------------------------------------------
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            import bench_iteration
+            it = bench_iteration.measure(len(os.sched_getaffinity(0)))
+            line["iteration_wallclock"] = {
+                "unit": "s", "config": "pointmass.ini: 300 / 75 episodes, 750 candidates, M = 1000 cycles, B = 128",
+                "reference_s": [r["wall_s"] for r in it["reference"]], "b200_s": [g["wall_s"] for g in it["b200"]],
+                "reference_nets_s": [r["t_nets_s"] for r in it["reference"]],
+                "b200_nets_s": [g["t_nets_s"] for g in it["b200"]],
+                "to_cpu_s": [g["t_to_s"] for g in it["b200"]], "speedup_wall": it["speedup_wall"],
+                "speedup_nets": it["speedup_nets"], "workers": it["workers"],
+                "note": "iterations 2 and 3 (iteration 2 of the B200 arm includes engine set-up + graph capture)"}
+        except Exception as e:
+            line["iteration_wallclock"] = {"error": str(e)[:200]}
 
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -606,7 +635,7 @@ def main():
         dist.destroy_process_group()
 
 
-def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
+def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None, H=HIDDEN, K=10):
     """One Sobolev critic update per step (fused gather + target forward + Sobolev
     loss with double backprop + fold + Adam + Polyak), data-parallel over ranks:
     every rank draws the same global index stream and takes its B-row slice (weak
@@ -619,7 +648,13 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
     from paper_2602_19699_b200.device import DeviceNet
     from paper_2602_19699_b200.buffer import ReplayBuffer, SampleBatch
     spec, _ = specs.config("manipulator3")
-    actor, critic, std = make_nets(spec)
+    if H == HIDDEN:
+        actor, critic, std = make_nets(spec)
+    else:
+        from paper_2602_19699_b200 import nets as B_nets
+        c, h = specs.normalisation(spec)
+        critic = B_nets.init_mlp([spec.n + 1, H, H, H, 1], np.random.default_rng(np.random.SeedSequence([SEED, 0])),
+                                 in_center=c, in_half=h)
     net = DeviceNet(critic)
     tgt = DeviceNet(critic)
     cap = 1 << 20
@@ -658,7 +693,6 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    K = 10
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(K):
@@ -670,7 +704,7 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    H, d = HIDDEN, spec.n + 1
+    d = spec.n + 1
     f = 28 * H * H + 14 * d * H + 8 * H
     peak, peak_source = tensor_peak()
     ach = f * B / (ms * 1e-3) / 1e12
@@ -683,8 +717,7 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None):
                          "kernel": "the whole update (critic_tc_kernel per-sample stage on tcgen05 + reduction "
                                    "GEMMs + fold/Adam/Polyak), algorithmic F_critic = 28H^2+14dH+8H per sample"},
             "includes": "fused gather + target forward + Sobolev fwd/double-backprop + fold + "
-                        + ("Adam + Polyak" if world == 1 else "NCCL all-reduce of the gradient + Adam + Polyak"),
-            "sweep": "profiles/critic_sweep.py (batch 4k-1M x hidden 64-512, 1 GPU)"}
+                        + ("Adam + Polyak" if world == 1 else "NCCL all-reduce of the gradient + Adam + Polyak")}
 
 
 if __name__ == "__main__":

@@ -42,7 +42,15 @@ def main():
     ap.add_argument("--max-iter-later", type=int, default=10)
     ap.add_argument("--precision", default="fp32")
     args = ap.parse_args()
+    print(json.dumps(measure(args.workers, args.m_updates, args.max_iter_first, args.max_iter_later,
+                             args.precision)), flush=True)
 
+
+def measure(workers, m_updates=1000, max_iter_first=20, max_iter_later=10, precision="fp32"):
+    """The iteration wall-clock line (also embedded by bench.py as `iteration_wallclock`)."""
+    from types import SimpleNamespace
+    args = SimpleNamespace(workers=workers, m_updates=m_updates, max_iter_first=max_iter_first,
+                           max_iter_later=max_iter_later, precision=precision)
     import trajrl
     import trajrl.trainer as T
     import paper_2602_19699_b200 as P
@@ -92,7 +100,7 @@ def main():
                        "minibatch": 128, "hidden": [64, 64, 64], "max_iter": [args.max_iter_first,
                                                                            args.max_iter_later],
                        "eval_use_to": False}}
-    print(json.dumps(line), flush=True)
+    return line
 
 
 if __name__ == "__main__":
