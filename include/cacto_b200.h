@@ -180,6 +180,10 @@ int cacto_rollout_score(const cacto_system_t* sys, const cacto_cost_t* cost, con
 /* dst[i, r] = src[r, idx[i]] for r < R, i < K: src [R, N] (dtype), dst [K, R] */
 int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int64_t N, const int64_t* idx, int64_t K,
                        void* dst, void* stream);
+/* dst[i, :] = src[idx[i], :], rows of R elements (dtype): the kept warm starts of a
+ * start-major [N, T, m] U (trainer.py:192-193), one coalesced row copy each */
+int cacto_take_rows(int32_t dtype, const void* src, int64_t R, const int64_t* idx, int64_t K, void* dst,
+                    void* stream);
 
 /* -- (a6, a8) BIC scores: std sigma(x0) (trainer.py:150-151), gap
  * |V(x0) - J(x0)| or sigma * gap (north_star).

@@ -94,6 +94,7 @@ SIGNATURES = {
     "cacto_rollout_ex": (ctypes.c_int, [_PSYS, _PCOST, _PMLP, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P, _P,
                                          _P]),
     "cacto_take_columns": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64, _P, _P]),
+    "cacto_take_rows": (ctypes.c_int, [_I32, _P, _I64, _P, _I64, _P, _P]),
     "cacto_rollout_score": (ctypes.c_int, [_PSYS, _PCOST, _PMLP, _I32, _PMLP, _PMLP, _P, _I32, _I64, _I32, _I32,
                                             _P, _P, _P, _P]),
     "cacto_score": (ctypes.c_int, [_I32, _PMLP, _PMLP, _P, _P, _I64, _P, _P]),

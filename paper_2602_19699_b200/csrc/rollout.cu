@@ -212,7 +212,40 @@ __global__ void take_columns_kernel(const T* __restrict__ src, int64_t R, int64_
     dst[e] = src[rr * N + idx[i]];
   }
 }
+// dst[i, :] = src[idx[i], :] for rows of R elements: one warp per row, 16-byte
+// vectors when the rows allow (the kept warm starts of a start-major U)
+template <typename T>
+__global__ void take_rows_kernel(const T* __restrict__ src, int64_t R, const int64_t* __restrict__ idx, int64_t K,
+                                 T* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (R * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0;
+  for (int64_t i = w0; i < K; i += nw) {
+    const int64_t r = idx[i];
+    if (vec) {
+      const int64_t nv = R * (int64_t)sizeof(T) / 16;
+      const float4* s4 = reinterpret_cast<const float4*>(src + r * R);
+      float4* d4 = reinterpret_cast<float4*>(dst + i * R);
+      for (int64_t v = lane; v < nv; v += 32) d4[v] = __ldg(s4 + v);
+    } else {
+      for (int64_t e = lane; e < R; e += 32) dst[i * R + e] = src[r * R + e];
+    }
+  }
+}
 }  // namespace cacto
+
+extern "C" int cacto_take_rows(int32_t dtype, const void* src, int64_t R, const int64_t* idx, int64_t K, void* dst,
+                               void* stream) {
+  if (R < 0 || K < 0 || (R * K > 0 && (!src || !idx || !dst))) return set_error(CACTO_EVALUE, "take_rows: bad arguments");
+  if (R * K == 0) return CACTO_OK;
+  unsigned grid = (unsigned)std::min<int64_t>((K + 7) / 8, 16 * (int64_t)num_sms());
+  if (dtype == CACTO_F32)
+    take_rows_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)src, R, idx, K, (float*)dst);
+  else
+    take_rows_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)src, R, idx, K, (double*)dst);
+  return check_launch("take_rows_kernel");
+}
 
 extern "C" int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int64_t N, const int64_t* idx, int64_t K,
                                   void* dst, void* stream) {

@@ -32,30 +32,7 @@ CACTO_D void mbar_wait(uint64_t* bar, uint32_t parity) {
 // same, with a suspend-time hint: the waiting warp sleeps until the phase
 // completes (or the hint expires) instead of re-polling, leaving issue slots
 // to the warps that share its scheduler
-#ifndef CACTO_WAIT_MODE
-#define CACTO_WAIT_MODE 0
-#endif
-#ifndef CACTO_WAIT_NS
-#define CACTO_WAIT_NS 64
-#endif
 CACTO_D void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-#if CACTO_WAIT_MODE == 1
-  // plain try_wait (system time limit)
-  mbar_wait(bar, parity);
-  return;
-#elif CACTO_WAIT_MODE == 2
-  // test_wait, then back off with nanosleep between polls
-  uint32_t ok = 0;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(saddr(bar)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    __nanosleep(CACTO_WAIT_NS);
-  }
-#endif
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"

@@ -20,6 +20,17 @@ from .device import DeviceNet, abi_dtype, device, device_net, to_device, torch_d
 from .nets import actor_rollout_batch
 
 
+import os
+
+# layout of the cost rollout's kept controls: time-major [T, m, N] (K1's per-step
+# writes coalesced; the warm-start take reads one 4-byte value per 32-byte sector)
+# or start-major [N, T, m] (take = one coalesced row copy per kept start, but
+# K1's 12-byte strided writes cost more than the take saves: measured manipulator3
+# step 4.12 -> 4.19 ms, dubins 0.83 -> 0.90 ms, profiles/README.md).
+# CACTO_WARM_TMAJOR=0 selects start-major (A/B only).
+_TMAJOR = os.environ.get("CACTO_WARM_TMAJOR", "1") == "1"
+
+
 def _stream():
     return torch.cuda.current_stream().cuda_stream
 
@@ -128,20 +139,25 @@ class BicPipeline:
         self.ws = SelectWorkspace()
         self.kernel_launches = 0
 
+    def _u_all(self, N, T, dt, dev):
+        """(pointer, flags) of the buffer the cost rollout writes every candidate's
+        controls into (start-major [N, T, m], or time-major under _TMAJOR)."""
+        shape = (T, self.model.m, N) if _TMAJOR else (N, T, self.model.m)
+        if getattr(self, "u_all", None) is None or tuple(self.u_all.shape) != shape or self.u_all.dtype != dt:
+            self.u_all = torch.empty(shape, device=dev, dtype=dt)
+        return self.u_all.data_ptr(), (_lib.ROLLOUT_U_TIME_MAJOR if _TMAJOR else 0)
+
     def rollout_costs(self, x0: torch.Tensor, t0: int = 0, keep_controls: bool = False) -> torch.Tensor:
         """K1 cost-to-go of every candidate; with keep_controls the same launch
-        also writes every candidate's controls time-major into self.u_all
-        [T, m, N], from which the kept warm starts are taken (no second rollout)."""
+        also writes every candidate's controls into self.u_all, from which the
+        kept warm starts are taken (no second rollout)."""
         N = x0.shape[0]
         dt = torch_dtype(self.precision)
         cost = torch.empty(N, device=x0.device, dtype=dt)
         T = self.model.t_max - t0
         U, flags = None, 0
         if keep_controls:
-            shape = (T, self.model.m, N)
-            if getattr(self, "u_all", None) is None or tuple(self.u_all.shape) != shape or self.u_all.dtype != dt:
-                self.u_all = torch.empty(shape, device=x0.device, dtype=dt)
-            U, flags = self.u_all.data_ptr(), _lib.ROLLOUT_U_TIME_MAJOR
+            U, flags = self._u_all(N, T, dt, x0.device)
         _lib.call("cacto_rollout_ex", self.sysd, self.costd, self.actor.desc, x0.data_ptr(), None, t0, N, T, flags,
                   U, None, None, cost.data_ptr(), _stream())
         return cost
@@ -156,10 +172,7 @@ class BicPipeline:
         T = self.model.t_max - t0
         U, flags = None, 0
         if keep_controls:
-            shape = (T, self.model.m, N)
-            if getattr(self, "u_all", None) is None or tuple(self.u_all.shape) != shape or self.u_all.dtype != dt:
-                self.u_all = torch.empty(shape, device=x0.device, dtype=dt)
-            U, flags = self.u_all.data_ptr(), _lib.ROLLOUT_U_TIME_MAJOR
+            U, flags = self._u_all(N, T, dt, x0.device)
         rc = _lib.load().cacto_rollout_score(
             self.sysd, self.costd, self.actor.desc, _lib.SCORE[self.mode], self.std.desc if self.std else None,
             self.critic.desc if self.critic else None, x0.data_ptr(), t0, N, T, flags, U, cost.data_ptr(),
@@ -200,8 +213,12 @@ class BicPipeline:
         if reuse:
             # the kept starts' controls from the cost rollout (same actor, start and t0:
             # the trajectories trainer.py:192-193 would roll out again)
-            _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
-                      N, sel.data_ptr(), K, U.data_ptr(), _stream())
+            if _TMAJOR:
+                _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
+                          N, sel.data_ptr(), K, U.data_ptr(), _stream())
+            else:
+                _lib.call("cacto_take_rows", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
+                          sel.data_ptr(), K, U.data_ptr(), _stream())
             return U, 1
         kept = x0.index_select(0, sel)
         _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, K, T,
