@@ -14,10 +14,13 @@
 //     weight gradients to HBM: [g_i ; zbar_i] and [u_i ; a_i] as 2B-row matrices.
 //  2. the batch reductions -- gW_i = [g_i ; zbar_i]^T [u_i ; a_i] as one tcgen05
 //     GEMM per layer over K = 2B (gemm_tc.cu, MN-major operands), bias and
-//     output-row gradients as deterministic column sums.  One gradient slot
+//     output-row gradients (a matrix-vector product: out_row_grad_kernel on the
+//     CUDA cores) as deterministic column sums.  One gradient slot
 //     (n_partials = 1), so the fold / Adam kernels apply unchanged.
 // TMEM (512 columns, one tile per CTA): D [64] | A_hi [32] | A_lo [32] |
 // z_0..z_2 [3 x 64] | g_i -> zeta_i [3 x 64].
+#include <algorithm>
+
 #include "tcmlp.cuh"
 
 namespace cacto {
@@ -48,7 +51,8 @@ constexpr uint32_t OFF_W0T = 2 * SLOT;          // hi, lo
 constexpr uint32_t OFF_W1T = OFF_W0T + 2 * W0T;
 constexpr uint32_t OFF_W2T = OFF_W1T + 2 * WHT;
 constexpr uint32_t OFF_W3 = OFF_W2T + 2 * WHT;  // fp32 output row w_3 [64], unscaled
-constexpr uint32_t BYTES = OFF_W3 + HP * 4 + 1024;
+constexpr uint32_t IMG_BYTES = OFF_W3 + HP * 4;  // the staged weights (a multiple of 16 B)
+constexpr uint32_t BYTES = IMG_BYTES + 1024;
 
 struct CBatch {
   const int64_t* idx;
@@ -77,6 +81,7 @@ struct Args {
   float* UA[4];  // UA[3]: u_3 rows then a_3 rows (the output row w_3)
   float* V3;     // [2B]: 1 on u_3 rows, -2 e_v on a_3 rows (left factor of gW_3, gb_3)
   float* lossp;  // [gridDim.x]
+  const unsigned char* img;  // pre-staged shared-memory image of the weights (or null)
 };
 
 // transposed copy: element (r = c, k = o) = W[o][c] * scale, K-major SW128 fp16
@@ -127,6 +132,39 @@ CACTO_D void st16g(float* dst, const float (&v)[16]) {
 
 }  // namespace ctc
 
+// the shared-memory image of one update's weights: critic + target forward slots
+// (scaled hi/lo fp16, K-major SW128), the transposed critic layers and w_3; written
+// by `tid` of `nthr` threads to `base` (shared memory, or the global image)
+template <int ACT>
+CACTO_D void critic_stage_all(unsigned char* base, const ctc::Args& a, int tid, int nthr) {
+  using namespace ctc;
+  using AF = ActTC<ACT>;
+  constexpr float S = AF::S;
+  const int ip = a.ip;
+  const int d = a.b.n + 1;
+  if (ip == 8) {
+    stage_net<HP, 8, AF>(base, a.critic, 3, d, 1, tid, nthr);
+    if (a.target) stage_net<HP, 8, AF>(base + SLOT, a.target, 3, d, 1, tid, nthr);
+  } else {
+    stage_net<HP, 16, AF>(base, a.critic, 3, d, 1, tid, nthr);
+    if (a.target) stage_net<HP, 16, AF>(base + SLOT, a.target, 3, d, 1, tid, nthr);
+  }
+  const float* W0 = a.critic;
+  const float* W1 = W0 + HP * ip + HP;
+  const float* W2 = W1 + HP * HP + HP;
+  const float* W3 = W2 + HP * HP + HP;
+  stage_wt(base + OFF_W0T, base + OFF_W0T + W0T, W0, HP, d, ip, S, rtc::NOUT, tid, nthr);
+  stage_wt(base + OFF_W1T, base + OFF_W1T + WHT, W1, HP, HP, HP, S, HP, tid, nthr);
+  stage_wt(base + OFF_W2T, base + OFF_W2T + WHT, W2, HP, HP, HP, S, HP, tid, nthr);
+  float* w3 = reinterpret_cast<float*>(base + OFF_W3);
+  for (int c = tid; c < HP; c += nthr) w3[c] = W3[c];
+}
+
+template <int ACT>
+__global__ void critic_tc_image_kernel(const ctc::Args a, unsigned char* img) {
+  critic_stage_all<ACT>(img, a, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
 template <int ACT>
 __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args a) {
   using namespace ctc;
@@ -147,28 +185,33 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
   __shared__ float red[NTHR / 32];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ip = a.ip;
   const int n = a.b.n;
   const int d = n + 1;
 
-  // ---- weights -> shared memory ----------------------------------------------------
-  if (ip == 8) {
-    stage_net<HP, 8, AF>(base, a.critic, 3, d, 1, threadIdx.x, NTHR);
-    if (a.target) stage_net<HP, 8, AF>(base + SLOT, a.target, 3, d, 1, threadIdx.x, NTHR);
+  // ---- weights -> shared memory: one bulk copy of the image critic_tc_image_kernel
+  //      built for this update (the per-CTA fp16 split + swizzle staging cost ~11 % of
+  //      the kernel's stall samples), or stage it here -------------------------------
+  if (a.img) {
+    __shared__ __align__(8) uint64_t img_bar;
+    if (threadIdx.x == 0) {
+      tc::mbar_init(&img_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc::mbar_expect_tx(&img_bar, IMG_BYTES);
+      for (uint32_t o = 0; o < IMG_BYTES; o += 32768) {
+        const uint32_t sz = IMG_BYTES - o < 32768 ? IMG_BYTES - o : 32768;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                saddr(base + o)),
+            "l"(a.img + o), "r"(sz), "r"(saddr(&img_bar))
+            : "memory");
+      }
+    }
+    tc::mbar_wait(&img_bar, 0);
   } else {
-    stage_net<HP, 16, AF>(base, a.critic, 3, d, 1, threadIdx.x, NTHR);
-    if (a.target) stage_net<HP, 16, AF>(base + SLOT, a.target, 3, d, 1, threadIdx.x, NTHR);
-  }
-  {
-    const float* W0 = a.critic;
-    const float* W1 = W0 + HP * ip + HP;
-    const float* W2 = W1 + HP * HP + HP;
-    const float* W3 = W2 + HP * HP + HP;
-    stage_wt(base + OFF_W0T, base + OFF_W0T + W0T, W0, HP, d, ip, S, rtc::NOUT, threadIdx.x, NTHR);
-    stage_wt(base + OFF_W1T, base + OFF_W1T + WHT, W1, HP, HP, HP, S, HP, threadIdx.x, NTHR);
-    stage_wt(base + OFF_W2T, base + OFF_W2T + WHT, W2, HP, HP, HP, S, HP, threadIdx.x, NTHR);
-    float* w3 = reinterpret_cast<float*>(base + OFF_W3);
-    for (int c = threadIdx.x; c < HP; c += NTHR) w3[c] = W3[c];
+    critic_stage_all<ACT>(base, a, threadIdx.x, NTHR);
   }
   if (threadIdx.x == 0) {
     tc::mbar_init(&full_bar, NEPI);
@@ -337,6 +380,18 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       put_input(xin);
       preload_bias(TZ, bias_c, 0);
       handoff();
+      // L2 prefetch of this CTA's next tile's sample rows (issued while the first
+      // layers' MMAs run): the gather at the next tile start then hits L2
+      if (owner) {
+        const int64_t gbn = (t + gridDim.x) * TILE + r;
+        if (gbn < B) {
+          const int64_t rn = a.b.row(gbn);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.b.xa + rn * d));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.b.v_bar_x + rn * n));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.b.v_bar + rn));
+          if (boot) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.b.xa_plus_k + rn * d));
+        }
+      }
       for (int l = 0; l < 3; ++l) {
         if (boot) {
           wait_done_t();
@@ -588,7 +643,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
 namespace ctc {
 
 struct Plan2 {  // workspace carve
-  size_t off_gz[3], off_ua[4], off_v3, off_lossp, off_part[4], part_bytes[4], total;
+  size_t off_gz[3], off_ua[4], off_v3, off_lossp, off_img, off_part[4], part_bytes[4], total;
 };
 
 static Plan2 plan2(int64_t B, int64_t P) {
@@ -604,12 +659,15 @@ static Plan2 plan2(int64_t B, int64_t P) {
   for (int l = 1; l < 4; ++l) p.off_ua[l] = take((size_t)2 * B * 68 * 4);
   p.off_v3 = take((size_t)2 * B * 4 + 16);
   p.off_lossp = take((size_t)4096 * 4);
+  p.off_img = take(IMG_BYTES);
   // split-K partials of the four reduction GEMMs, each in its own region (the fused
   // reduce + scatter reads all four after the last GEMM)
   const int pm[4] = {HP, HP, HP, 1}, pn[4] = {17, 65, 65, 65};
   for (int l = 0; l < 4; ++l) {
     const size_t w = gemm_workspace_bytes(pm[l], pn[l], (int)(2 * B));
-    const size_t one = (size_t)pm[l] * pn[l] * 4;
+    size_t one = (size_t)pm[l] * pn[l] * 4;
+    if (l == 3) one = (size_t)4 * 1024 * 65 * 4;  // out_row_grad_kernel: up to 4 x SMs partial rows
+    else one = std::max(one, (size_t)2048 * HP * pn[l] * 4);  // wgrad_kernel: 2 partials per CTA
     p.part_bytes[l] = w > one ? w : one;
     p.off_part[l] = take(p.part_bytes[l]);
   }
@@ -665,6 +723,286 @@ __global__ void reduce_scatter_grads_kernel(const PartSet ps, int cols0, float* 
   if (lane == 0) slot[dst] += s;
 }
 
+// ---- weight gradients of layers 0..2 on the tensor cores, fp16 pairs -----------------
+// gW_l[o][c] = alpha * sum_b G_l[b][o] * U_l[b][c] over the 2B rows b (g then zbar in G,
+// u then a | bias column in U): the per-sample factors critic_tc_kernel streamed as fp32
+// [2B][w] rows.  Per 64-sample k-block:
+//   warp 16      TMA: the raw fp32 [64][64] G block and [64][w] U block -> a 3-stage ring
+//   warps 0..15  read the raw block from shared memory, scale by SB, split each value into
+//                fp16 hi + lo (as the per-sample MMAs do) and store them TRANSPOSED into
+//                K-major SW128 tiles (row = o or c, 64 samples = 128 B), a 2-stage ring
+//   warp 17      issues [G_hi ; G_lo] x U_hi and [G_hi ; G_lo] x U_lo (tcgen05 kind::f16,
+//                M = 128: rows 0..63 take the hi parts of G, rows 64..127 the lo parts,
+//                N = 32 / 80) into one TMEM accumulator: two MMAs per k-step and no padded
+//                rows; the two row halves leave as two partials that the reduction sums
+// Each factor is read from HBM once (the 3xTF32 GEMM it replaces split operands through
+// shared memory at ~2.3 TB/s).  CTAs split K per layer; the partials go to
+// reduce_scatter_grads_kernel (fixed order: deterministic).
+constexpr int WG_KB = 64;
+constexpr int WG_RAW = 3;    // raw fp32 stages
+constexpr int WG_STAGES = 3; // converted fp16 stages
+constexpr int WG_CONV = 16;
+constexpr int WG_TMA_WARP = WG_CONV, WG_MMA_WARP = WG_CONV + 1;
+constexpr int WG_THREADS = (WG_CONV + 2) * 32;
+constexpr uint32_t WG_A = 128 * 128;  // [G_hi ; G_lo]: 128 rows x 64 samples (fp16)
+constexpr uint32_t WG_B = 80 * 128;
+constexpr uint32_t WG_STAGE = WG_A + 2 * WG_B;
+constexpr uint32_t WG_RG = WG_KB * 64 * 4;   // raw G block
+constexpr uint32_t WG_RU = WG_KB * 68 * 4;   // raw U block (widest row: 68 floats)
+constexpr uint32_t WG_RSTAGE = WG_RG + WG_RU;
+constexpr uint32_t WG_SMEM = WG_STAGES * WG_STAGE + WG_RAW * WG_RSTAGE + 1024;
+constexpr float WG_SB = 16.f;
+
+struct __align__(64) WgradArgs {
+  CUtensorMap tg[3], tu[3];  // raw G / U blocks: boxes [64][64] and [64][uw]
+  int uw[3], ncol[3], nmma[3];
+  int cta0[4];
+  int64_t chunk[3];
+  int64_t K2;
+  float* part[3];
+  float alpha;
+};
+
+// 8 K-consecutive values of one row -> hi / lo fp16 16-byte chunks
+CACTO_D void split8(const float (&v)[8], uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) rtc::split2(v[2 * j] * WG_SB, v[2 * j + 1] * WG_SB, h[j], l[j]);
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+CACTO_D void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+CACTO_D float lds1f(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+__global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_constant__ WgradArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t raw_full[WG_RAW], raw_empty[WG_RAW], full_bar[WG_STAGES], empty_bar[WG_STAGES],
+      acc_bar;
+  __shared__ uint32_t tmem_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = blockIdx.x >= a.cta0[2] ? 2 : (blockIdx.x >= a.cta0[1] ? 1 : 0);
+  const int z = blockIdx.x - a.cta0[l];
+  const int64_t k0 = (int64_t)z * a.chunk[l];
+  const int64_t k1 = k0 + a.chunk[l] < a.K2 ? k0 + a.chunk[l] : a.K2;
+  const int nkb = (int)((k1 - k0 + WG_KB - 1) / WG_KB);
+  const int ncol = a.ncol[l], uw = a.uw[l];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < WG_RAW; ++s) {
+      tc::mbar_init(&raw_full[s], 1);
+      tc::mbar_init(&raw_empty[s], WG_CONV);
+    }
+    for (int s = 0; s < WG_STAGES; ++s) {
+      tc::mbar_init(&full_bar[s], WG_CONV);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    tc::mbar_init(&acc_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == WG_MMA_WARP) tc::tmem_alloc(&tmem_sh, 128);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+  const uint32_t sb = saddr(base);
+  unsigned char* raw = base + WG_STAGES * WG_STAGE;
+  const uint32_t rsb = saddr(raw);
+
+  if (warp == WG_TMA_WARP) {
+    if (lane == 0) {
+      const uint32_t ub = (uint32_t)(WG_KB * uw * 4);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % WG_RAW;
+        if (kb >= WG_RAW) tc::mbar_wait(&raw_empty[s], ((kb / WG_RAW) - 1) & 1);
+        tc::mbar_expect_tx(&raw_full[s], WG_RG + ub);
+        const int row = (int)(k0 + (int64_t)kb * WG_KB);
+        unsigned char* rs = raw + (uint32_t)s * WG_RSTAGE;
+        tc::tma_load_2d(rs, &a.tg[l], &raw_full[s], 0, row);
+        tc::tma_load_2d(rs + WG_RG, &a.tu[l], &raw_full[s], 0, row);
+      }
+    }
+  } else if (warp < WG_CONV) {
+    // warps 0..7 convert G, warps 8..15 U: warp w handles samples [8(w%8), +8) of every
+    // k-block; lane L owns rows L, L+32 (and L+64 of U) -- 8 consecutive samples of a
+    // row = one 16-byte chunk of the K-major tile
+    const bool gw = warp < 8;
+    const int sg = warp & 7;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int rs = kb % WG_RAW, s = kb % WG_STAGES;
+      tc::mbar_wait(&raw_full[rs], (kb / WG_RAW) & 1);
+      float v[3][8];
+      const uint32_t rb = rsb + (uint32_t)rs * WG_RSTAGE;
+      const int64_t b0 = k0 + (int64_t)kb * WG_KB + sg * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool ok = b0 + j < k1;  // rows past K2 are TMA zero fill; past k1 belong to the next CTA
+        const int sj = sg * 8 + j;
+        if (gw) {
+          v[0][j] = ok ? lds1f(rb + (uint32_t)(sj * 64 + lane) * 4) : 0.f;
+          v[1][j] = ok ? lds1f(rb + (uint32_t)(sj * 64 + lane + 32) * 4) : 0.f;
+        } else {
+#pragma unroll
+          for (int rr = 0; rr < 3; ++rr) {
+            const int c = lane + 32 * rr;
+            v[rr][j] = (ok && c < ncol) ? lds1f(rb + WG_RG + (uint32_t)(sj * uw + c) * 4) : 0.f;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&raw_empty[rs]);
+      if (kb >= WG_STAGES) tc::mbar_wait(&empty_bar[s], ((kb / WG_STAGES) - 1) & 1);
+      const uint32_t st0 = sb + (uint32_t)s * WG_STAGE;
+      uint4 hi, lo;
+      if (gw) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int o = lane + 32 * rr, ol = o + 64;  // hi -> row o, lo -> row o + 64
+          split8(v[rr], hi, lo);
+          sts128(st0 + (uint32_t)o * 128 + (uint32_t)((sg ^ (o & 7)) << 4), hi);
+          sts128(st0 + (uint32_t)ol * 128 + (uint32_t)((sg ^ (ol & 7)) << 4), lo);
+        }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+          const int c = lane + 32 * rr;
+          if (c < ncol) {
+            split8(v[rr], hi, lo);
+            const uint32_t off = (uint32_t)c * 128 + (uint32_t)((sg ^ (c & 7)) << 4);
+            sts128(st0 + WG_A + off, hi);
+            sts128(st0 + WG_A + WG_B + off, lo);
+          }
+        }
+      }
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full_bar[s]);
+    }
+    if (warp < 4) {  // accumulator rows 0..63 (hi x U) -> partial 2z, rows 64..127 (lo x U) -> 2z + 1
+      tc::mbar_wait(&acc_bar, 0);
+      tc::tc_fence_after();
+      const int row = warp * 32 + lane, orow = row & 63;
+      float* dst = a.part[l] + ((int64_t)(2 * z + (row >> 6)) * HP + orow) * ncol;
+      for (int c0 = 0; c0 < ncol; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16_wait(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c0 + c < ncol) dst[c0 + c] = a.alpha * v[c];
+      }
+    }
+  } else {
+    // MMA issuer
+    const uint32_t idesc = tc::idesc_f16(a.nmma[l]);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % WG_STAGES;
+      tc::mbar_wait(&full_bar[s], (kb / WG_STAGES) & 1);
+      tc::tc_fence_after();
+      const uint32_t st0 = sb + (uint32_t)s * WG_STAGE;
+#pragma unroll
+      for (int kk = 0; kk < WG_KB / 16; ++kk) {
+        const uint64_t ad = tc::make_desc(st0 + kk * 32, 16, 1024, 2);
+        const uint64_t bhi = tc::make_desc(st0 + WG_A + kk * 32, 16, 1024, 2);
+        const uint64_t blo = tc::make_desc(st0 + WG_A + WG_B + kk * 32, 16, 1024, 2);
+        tc::mma_f16_ss_elect(tmem, ad, bhi, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+        tc::mma_f16_ss_elect(tmem, ad, blo, idesc, 1u);
+      }
+      tc::tc_commit_elect(&empty_bar[s]);
+      __syncwarp();
+    }
+    tc::tc_commit_elect(&acc_bar);
+    __syncwarp();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == WG_MMA_WARP) tc::tmem_dealloc(tmem, 128);
+}
+
+// 2D fp32 tensor map (no swizzle) over rows x cols with a row stride of `ld` floats
+typedef CUresult (*WgEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static int wg_map(CUtensorMap* map, const float* X, int64_t rows, int cols, int ld, int box_rows) {
+  static WgEncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return set_error(CACTO_ECUDA, "wgrad: cuTensorMapEncodeTiled unavailable");
+    fn = (WgEncodeFn)p;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows}, strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)cols, (cuuint32_t)box_rows}, estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)X, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(CACTO_ECUDA, "wgrad: tensor map encode failed (%d)", (int)r);
+  return CACTO_OK;
+}
+
+// output-row gradient (w_3 and b_3): part[z][c] = alpha * sum_{b in chunk z} V3[b] * UA3[b][c],
+// c < 65, over the 2B rows [u_3 ; a_3 | bias column] -- a matrix-vector product, so
+// CUDA cores at HBM speed (one warp per row, lanes over columns; the 8 warps' sums
+// folded in a fixed order: deterministic)
+__global__ void __launch_bounds__(256) out_row_grad_kernel(const float* __restrict__ V3, const float* __restrict__ UA3,
+                                                           int64_t K2, int64_t chunk, float alpha, float* part) {
+  __shared__ float red[8][68];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = b0 + chunk < K2 ? b0 + chunk : K2;
+  // a half-warp per row (17 lanes x float4 = the 68-float row), two rows per warp
+  // step and 4 steps in flight: 8 independent row loads per warp before the FMAs
+  const int h = lane >> 4, c4 = lane & 15;  // row parity, float4 column (lanes 0..15 -> cols 0..63)
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float accb = 0.f;  // column 64 (bias), lane c4 == 0 of each half
+  for (int64_t b = b0 + 2 * warp + h; b < b1; b += 4 * 16) {
+    float v[4];
+    float4 x[4];
+    float xb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t r = b + u * 16;
+      const bool ok = r < b1;
+      v[u] = ok ? V3[r] : 0.f;
+      x[u] = ok ? *reinterpret_cast<const float4*>(UA3 + r * 68 + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      xb[u] = (ok && c4 == 0) ? UA3[r * 68 + 64] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc.x = fmaf(v[u], x[u].x, acc.x);
+      acc.y = fmaf(v[u], x[u].y, acc.y);
+      acc.z = fmaf(v[u], x[u].z, acc.z);
+      acc.w = fmaf(v[u], x[u].w, acc.w);
+      accb = fmaf(v[u], xb[u], accb);
+    }
+  }
+  // the two half-warps' row sums, then the 8 warps in a fixed order
+  acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+  acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+  acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 16);
+  acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 16);
+  accb += __shfl_xor_sync(0xffffffffu, accb, 16);
+  if (h == 0) {
+    red[warp][4 * c4] = acc.x;
+    red[warp][4 * c4 + 1] = acc.y;
+    red[warp][4 * c4 + 2] = acc.z;
+    red[warp][4 * c4 + 3] = acc.w;
+    if (c4 == 0) red[warp][64] = accb;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 65; c += 256) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w][c];
+    part[(int64_t)blockIdx.x * 65 + c] = alpha * t;
+  }
+}
+
 // loss partials of the per-tile CTAs -> one value; a fixed strided order per
 // thread and a fixed shuffle / shared-memory tree (deterministic)
 __global__ void loss_fold_kernel(const float* __restrict__ part, int n, float* dst) {
@@ -683,6 +1021,11 @@ __global__ void loss_fold_kernel(const float* __restrict__ part, int n, float* d
 }
 
 }  // namespace ctc
+
+static bool wgrad_enabled() {
+  const char* e = getenv("CACTO_CRITIC_WGRAD");  // 0: the 3xTF32 GEMM reductions (A/B measurements)
+  return !e || atoi(e) != 0;
+}
 
 bool critic_tc_enabled() {
   const char* e = getenv("CACTO_CRITIC_TC");  // 0: fused SIMT kernel (A/B measurements)
@@ -743,6 +1086,11 @@ int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_bat
   a.lossp = (float*)(w + p.off_lossp);
   const int64_t ntiles = (B + TILE - 1) / TILE;
   const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+  a.img = (const unsigned char*)(w + p.off_img);
+  if (c->activation == CACTO_ACT_ELU)
+    critic_tc_image_kernel<CACTO_ACT_ELU><<<32, 256, 0, st>>>(a, (unsigned char*)(w + p.off_img));
+  else
+    critic_tc_image_kernel<CACTO_ACT_TANH><<<32, 256, 0, st>>>(a, (unsigned char*)(w + p.off_img));
   auto kern = c->activation == CACTO_ACT_ELU ? critic_tc_kernel<CACTO_ACT_ELU> : critic_tc_kernel<CACTO_ACT_TANH>;
   if (!ensure_smem((const void*)kern, BYTES))
     return set_error(CACTO_ECUDA, "critic_loss(tc): %u B of shared memory not available", BYTES);
@@ -756,19 +1104,62 @@ int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_bat
   const int ncol[4] = {17, 65, 65, 65};
   const int wpad[4] = {20, 68, 68, 68};
   ctc::PartSet ps{};
-  for (int l = 0; l < 3; ++l) {
-    ps.p[l] = (const float*)(w + p.off_part[l]);
-    ps.stride[l] = (int64_t)HP * ncol[l];
-    rc = gemm_tf32_partials(HP, ncol[l], (int)(2 * B), a.GZ[l], 1, HP, a.UA[l], 1, wpad[l], a.inv_denom, 3,
-                            w + p.off_part[l], p.part_bytes[l], &ps.splits[l], st);
+  if (wgrad_enabled()) {
+    // layers 0..2: wgrad_kernel, one wave of CTAs split by HBM bytes per layer
+    ctc::WgradArgs g{};
+    const int64_t K2 = 2 * B;
+    const double bytes[3] = {64.0 + 17.0, 64.0 + 65.0, 64.0 + 65.0};
+    const int sms = num_sms();
+    int c0 = 0;
+    for (int l = 0; l < 3; ++l) {
+      rc = ctc::wg_map(&g.tg[l], a.GZ[l], K2, HP, HP, ctc::WG_KB);
+      if (!rc) rc = ctc::wg_map(&g.tu[l], a.UA[l], K2, wpad[l], wpad[l], ctc::WG_KB);
+      if (rc) return rc;
+      g.uw[l] = wpad[l];
+      g.ncol[l] = ncol[l];
+      g.nmma[l] = l == 0 ? 32 : 80;
+      int S = (int)(sms * bytes[l] / (bytes[0] + bytes[1] + bytes[2]));
+      if (S < 1) S = 1;
+      int64_t chunk = (K2 + S - 1) / S;
+      chunk = (chunk + ctc::WG_KB - 1) / ctc::WG_KB * ctc::WG_KB;
+      S = (int)((K2 + chunk - 1) / chunk);
+      g.chunk[l] = chunk;
+      g.cta0[l] = c0;
+      c0 += S;
+      g.part[l] = (float*)(w + p.off_part[l]);
+      ps.p[l] = g.part[l];
+      ps.stride[l] = (int64_t)HP * ncol[l];
+      ps.splits[l] = 2 * S;  // hi-row and lo-row partials of every CTA
+    }
+    g.cta0[3] = c0;
+    g.K2 = K2;
+    g.alpha = a.inv_denom / (ctc::WG_SB * ctc::WG_SB);
+    if (!ensure_smem((const void*)ctc::wgrad_kernel, ctc::WG_SMEM))
+      return set_error(CACTO_ECUDA, "critic_loss(tc): wgrad shared memory not available");
+    ctc::wgrad_kernel<<<c0, ctc::WG_THREADS, ctc::WG_SMEM, st>>>(g);
+    rc = check_launch("wgrad_kernel");
     if (rc) return rc;
+  } else {
+    for (int l = 0; l < 3; ++l) {
+      ps.p[l] = (const float*)(w + p.off_part[l]);
+      ps.stride[l] = (int64_t)HP * ncol[l];
+      rc = gemm_tf32_partials(HP, ncol[l], (int)(2 * B), a.GZ[l], 1, HP, a.UA[l], 1, wpad[l], a.inv_denom, 3,
+                              w + p.off_part[l], p.part_bytes[l], &ps.splits[l], st);
+      if (rc) return rc;
+    }
   }
   const int64_t K2 = 2 * B;
   ps.p[3] = (const float*)(w + p.off_part[3]);
   ps.stride[3] = 65;
-  rc = gemm_tf32_partials(1, 65, (int)K2, a.V3, (K2 + 3) / 4 * 4, 1, a.UA[3], 1, 68, a.inv_denom, 3,
-                          w + p.off_part[3], p.part_bytes[3], &ps.splits[3], st);
-  if (rc) return rc;
+  {
+    int S = 4 * num_sms();
+    const int64_t maxS = (int64_t)(p.part_bytes[3] / (65 * 4));
+    if (S > maxS) S = (int)maxS;
+    const int64_t chunk = (K2 + S - 1) / S;
+    S = (int)((K2 + chunk - 1) / chunk);
+    ctc::out_row_grad_kernel<<<S, 256, 0, st>>>(a.V3, a.UA[3], K2, chunk, a.inv_denom, (float*)(w + p.off_part[3]));
+    ps.splits[3] = S;
+  }
   const int items = ctc::scatter_items(lo.cols[0]);
   ctc::reduce_scatter_grads_kernel<<<(items * 32 + 255) / 256, 256, 0, st>>>(
       ps, lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1], lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);

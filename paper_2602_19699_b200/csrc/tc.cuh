@@ -120,6 +120,17 @@ CACTO_D void mma_f16_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uin
       : "memory");
 }
 
+// kind::f16 MMA with both operands in shared memory (K-major descriptors)
+CACTO_D void mma_f16_ss_elect(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // TMEM allocation (one warp, .sync.aligned) / release
 CACTO_D void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(dst_smem)), "r"(ncols)
