@@ -297,6 +297,15 @@ int cacto_actor_loss(const cacto_mlp_t* actor, const cacto_mlp_t* critic, const 
                      void* workspace, size_t workspace_bytes, int32_t* n_partials, void* stream);
 int cacto_std_loss(const cacto_mlp_t* std_net, const cacto_mlp_t* critic, const cacto_batch_t* batch,
                    void* workspace, size_t workspace_bytes, int32_t* n_partials, void* stream);
+/* std loss (nets.py:337-353) from precomputed errors err = v_bar - V_critic(xa)
+ * (cacto_value_errors over the same rows); with batch->cycle the errors of the cycle
+ * are err + (*cycle) * batch->idx_stride (laid out like the index lists).  The update
+ * loop's std phase uses the final critic for all M cycles (trainer.py:227-233), so the
+ * critic forward of every cycle runs as ONE batched launch.  Narrow nets (hp <= 64);
+ * wide nets return CACTO_EUNSUPPORTED (use cacto_std_loss). */
+int cacto_value_errors(const cacto_mlp_t* critic, const cacto_batch_t* batch, void* err, void* stream);
+int cacto_std_loss_err(const cacto_mlp_t* std_net, const void* err, const cacto_batch_t* batch, void* workspace,
+                       size_t workspace_bytes, int32_t* n_partials, void* stream);
 /* live rows (t < t_max) of a batch -> live_rows[0] (device int64) */
 int cacto_count_live(const cacto_batch_t* batch, int64_t* live_rows, void* stream);
 /* fold the partials: grad [P] (dtype) and loss [1] (dtype) */
@@ -324,6 +333,14 @@ int cacto_reduce_adam_graph(int32_t dtype, const void* workspace, int32_t n_part
                             double tau, void* loss_base, void* stream);
 /* ++(*counter) on device (closes one captured update cycle) */
 int cacto_counter_tick(int64_t* counter, void* stream);
+/* span[i] = *base + i (i < k), then *base += k: one launch gives the k cycles of a
+ * captured chunk their counters (each cycle reads its own span slot) */
+int cacto_counter_span(int64_t* base, int64_t* span, int32_t k, void* stream);
+/* slot (*counter % ring_n) of a [ring_n][ld] device ring <-> vec [P] (P <= ld; save != 0:
+ * vec -> slot).  The pipelined update loop keeps the critic of every cycle this way so the
+ * actor chain can run one cycle behind the critic chain (trainer.py:211-225 order). */
+int cacto_ring_copy(int32_t dtype, void* ring, const int64_t* counter, int64_t ring_n, int64_t ld, int64_t P,
+                    void* vec, int32_t save, void* stream);
 
 /* -- (a7) device PCG64 replay of Generator.uniform starts (envs/__init__.py:119-121)
  * x[i, j] = lo[j] + (hi[j]-lo[j]) * uniform draw (first_row + i)*n + j of the stream

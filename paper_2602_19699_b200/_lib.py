@@ -124,6 +124,10 @@ SIGNATURES = {
     "cacto_reduce_adam_graph": (ctypes.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D,
                                                 _D, _P, _D, _P, _P]),
     "cacto_counter_tick": (ctypes.c_int, [_P, _P]),
+    "cacto_ring_copy": (ctypes.c_int, [_I32, _P, _P, _I64, _I64, _I64, _P, _I32, _P]),
+    "cacto_counter_span": (ctypes.c_int, [_P, _P, _I32, _P]),
+    "cacto_value_errors": (ctypes.c_int, [_PMLP, _PBATCH, _P, _P]),
+    "cacto_std_loss_err": (ctypes.c_int, [_PMLP, _P, _PBATCH, _P, _SZ, _PI32, _P]),
     "cacto_sample_states": (ctypes.c_int, [_U64, _U64, _U64, _U64, _I64, _I64, _I32, _P, _P, _P, _P]),
     "cacto_gemm_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
     "cacto_gemm_tf32": (ctypes.c_int, [_I32, _I32, _I32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I32,

@@ -139,6 +139,19 @@ __global__ void reduce_adam_graph_kernel(const T* __restrict__ ws, int n, int64_
 
 __global__ void counter_tick_kernel(int64_t* c) { *c += 1; }
 
+// ring slot (*counter % ring) of a [ring][P] buffer <-> a [P] vector
+template <typename T>
+__global__ void ring_copy_kernel(T* ring, const int64_t* counter, int64_t ring_n, int64_t ld, int64_t P, T* vec,
+                                 int save) {
+  T* slot = ring + (*counter % ring_n) * ld;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    if (save)
+      slot[i] = vec[i];
+    else
+      vec[i] = slot[i];
+  }
+}
+
 static unsigned grid_of(int64_t P) {
   int64_t b = (P + 255) / 256;
   int64_t cap = 8 * (int64_t)num_sms();
@@ -225,6 +238,31 @@ extern "C" int cacto_reduce_adam_graph(int32_t dtype, const void* workspace, int
         (const double*)workspace, n_partials, P, (double*)params, (double*)m, (double*)v, counter, step_base, bc1,
         bc2, lr, beta1, beta2, eps, 1.0 - beta1, 1.0 - beta2, (double*)target, 1.0 - tau, tau, (double*)loss_base);
   return check_launch("reduce_adam_graph_kernel");
+}
+
+extern "C" int cacto_ring_copy(int32_t dtype, void* ring, const int64_t* counter, int64_t ring_n, int64_t ld,
+                               int64_t P, void* vec, int32_t save, void* stream) {
+  if (!ring || !counter || !vec || ring_n < 1 || P < 0 || ld < P)
+    return set_error(CACTO_EVALUE, "ring_copy: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CACTO_F32)
+    ring_copy_kernel<float><<<grid_of(P), 256, 0, st>>>((float*)ring, counter, ring_n, ld, P, (float*)vec, save);
+  else
+    ring_copy_kernel<double><<<grid_of(P), 256, 0, st>>>((double*)ring, counter, ring_n, ld, P, (double*)vec, save);
+  return check_launch("ring_copy_kernel");
+}
+
+__global__ void counter_span_kernel(int64_t* base, int64_t* span, int k) {
+  const int64_t b = *base;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) span[i] = b + i;
+  __syncthreads();
+  if (threadIdx.x == 0) *base = b + k;
+}
+
+extern "C" int cacto_counter_span(int64_t* base, int64_t* span, int32_t k, void* stream) {
+  if (!base || !span || k < 1) return set_error(CACTO_EVALUE, "counter_span: bad arguments");
+  counter_span_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(base, span, k);
+  return check_launch("counter_span_kernel");
 }
 
 extern "C" int cacto_counter_tick(int64_t* counter, void* stream) {

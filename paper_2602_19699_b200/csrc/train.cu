@@ -350,7 +350,9 @@ struct VpArgs {
   int count_live;            // actor: count the live rows in-kernel (live_rows == null)
   T inv_denom;
   // std loss
-  const T* err;  // [rows] v_bar - V(xa)
+  const T* err;               // [rows] v_bar - V(xa)
+  const int64_t* err_cycle;   // optional: err += (*err_cycle) * err_stride (precomputed errors)
+  int64_t err_stride;
   // actor loss
   SysDev<T> sys;
   CostDev<T> cost;
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
           // nets.py:343-352
           T o = OUT[s];
           T sigma = head_value(a.head, a.nc, 0, o);
-          T e = a.err[base + s];
+          T e = a.err[(a.err_cycle ? (*a.err_cycle) * a.err_stride : 0) + base + s];
           term = (m_log(sigma) + T(0.5) * e * e / (sigma * sigma)) * inv_denom;
           T dl = (T(1) / sigma - e * e / (sigma * sigma * sigma)) * inv_denom;
           d[0] = dl * sigmoid(o);
@@ -768,6 +770,50 @@ static int std_entry(const cacto_mlp_t* sn, const cacto_mlp_t* cn, const cacto_b
   a.ws = (T*)ws;
   CACTO_VP_DISPATCH(T, VP_STD, 0, sh.hp, sh.ip, a, b->rows, n_partials, st);
   return set_error(CACTO_EUNSUPPORTED, "std_loss: hidden %d / input %d not built", sh.hp, sh.in);
+}
+
+// the std loss from precomputed errors e = v_bar - V(xa) (cacto_value_errors): the
+// update loop's std phase runs with the final critic, so every cycle's errors come
+// from ONE batched critic forward instead of one per cycle
+template <typename T>
+static int std_err_entry(const cacto_mlp_t* sn, const void* err, const cacto_batch_t* b, void* ws,
+                         int32_t* n_partials, cudaStream_t st) {
+  NetShape sh = shape_of(*sn);
+  VpArgs<T> a{};
+  a.nc = net_const<T>(*sn);
+  a.nh = sh.nh; a.in = sh.in; a.out = sh.out; a.act = sh.act; a.head = sh.head;
+  a.params = (const T*)sn->params;
+  a.off = offs_of(*sn);
+  a.b = batch_dev<T>(*b);
+  a.inv_denom = T(1) / (T)(b->denom > 0 ? b->denom : b->rows);
+  a.err = (const T*)err;
+  a.err_cycle = b->cycle;
+  a.err_stride = b->idx_stride;
+  a.ws = (T*)ws;
+  CACTO_VP_DISPATCH(T, VP_STD, 0, sh.hp, sh.ip, a, b->rows, n_partials, st);
+  return set_error(CACTO_EUNSUPPORTED, "std_loss: hidden %d / input %d not built", sh.hp, sh.in);
+}
+
+extern "C" int cacto_value_errors(const cacto_mlp_t* critic, const cacto_batch_t* batch, void* err, void* stream) {
+  int rc = validate_mlp(critic, "value_errors");
+  if (rc) return rc;
+  if (!batch || !err) return set_error(CACTO_EVALUE, "value_errors: null argument");
+  return cacto_forward_rows(critic, batch, /*err*/ 2, err, stream);
+}
+
+extern "C" int cacto_std_loss_err(const cacto_mlp_t* std_net, const void* err, const cacto_batch_t* batch,
+                                  void* workspace, size_t workspace_bytes, int32_t* n_partials, void* stream) {
+  int rc = validate_mlp(std_net, "std_loss");
+  if (rc) return rc;
+  if (!batch || batch->rows <= 0 || !err) return set_error(CACTO_EVALUE, "empty batch");
+  if (std_net->sizes[std_net->n_layers] != 1 || std_net->head != CACTO_HEAD_STD)
+    return set_error(CACTO_EVALUE, "std_loss: std net must have a scalar std head");
+  if (workspace_bytes < cacto_loss_workspace_bytes(std_net, batch->rows))
+    return set_error(CACTO_EVALUE, "std_loss: workspace too small");
+  if (is_wide(std_net)) return set_error(CACTO_EUNSUPPORTED, "std_loss_err: wide networks use cacto_std_loss");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (std_net->dtype == CACTO_F32) return std_err_entry<float>(std_net, err, batch, workspace, n_partials, st);
+  return std_err_entry<double>(std_net, err, batch, workspace, n_partials, st);
 }
 
 extern "C" int cacto_std_loss(const cacto_mlp_t* std_net, const cacto_mlp_t* critic, const cacto_batch_t* batch,

@@ -104,13 +104,16 @@ class UpdateEngine:
             import torch.distributed as dist
             if use_graphs and dist.get_backend(self.dp_group) != "nccl":
                 use_graphs = False  # only NCCL collectives can be captured in a CUDA graph
-        self.cnt = torch.zeros(2, device=dev, dtype=torch.int64)   # [critic/actor cycle, std cycle]
+        # cycle counters: [critic (and, unpipelined, actor), std, actor (pipelined)]
+        self.cnt = torch.zeros(3, device=dev, dtype=torch.int64)
         # bias-correction tables bc[t] = 1 - beta**t in Python double precision
         # (nets.py:380-381), grown on demand (_ensure_bc) so any run length works
         self.bc = {}
         self.max_steps = 0
         self._ensure_bc(max(int(max_steps), 1 + max(n.step for n in (self.actor, self.critic, self.std))))
         self.use_graphs = use_graphs
+        self.K = 16          # cycles per captured chunk (pipelined schedule)
+        self.cview = None
         self._graphs = None
         self._cap_M = 0
         self.idx = None
@@ -139,17 +142,18 @@ class UpdateEngine:
         self._graphs = None
 
     # -- one cycle, as kernel launches on the current stream -----------------------
-    def _batch(self, slot, whole=False):
-        """Batch descriptor of cycle `cnt[slot]`: this rank's slice of the global
-        list (or the whole list), losses averaged over the global minibatch."""
+    def _batch(self, slot, whole=False, cptr=None):
+        """Batch descriptor of index list `slot` at the cycle held by the device
+        counter `cptr` (default: cnt[slot]): this rank's slice of the global list (or
+        the whole list), losses averaged over the global minibatch."""
         lo, hi = (0, self.B) if whole else (self.lo, self.hi)
         d = self.buffer.ring_desc(self.idx[slot, :, lo:], rows=hi - lo)
-        d.cycle = self.cnt[slot:slot + 1].data_ptr()
+        d.cycle = self.cnt[slot:slot + 1].data_ptr() if cptr is None else cptr
         d.idx_stride = self.B
         d.denom = self.B if self.world > 1 else 0
         return d
 
-    def _adam(self, net: _Net, ws, npart, slot, target=None, loss=None):
+    def _adam(self, net: _Net, ws, npart, slot, target=None, loss=None, cptr=None):
         bc1, bc2 = self.bc[(net.beta1, net.beta2)]
         if self.world > 1:
             # fold -> [grad | loss] -> sum over ranks -> replicated Adam (+ Polyak)
@@ -158,8 +162,9 @@ class UpdateEngine:
                       g[net.dn.count:].data_ptr(), _stream())
             parallel.allreduce_grads(g, self.dp_group)
             ws, npart = g, 1
+        counter = self.cnt[slot:slot + 1].data_ptr() if cptr is None else cptr
         _lib.call("cacto_reduce_adam_graph", net.dn.desc.dtype, ws.data_ptr(), npart, net.dn.count,
-                  net.dn.params.data_ptr(), net.m.data_ptr(), net.v.data_ptr(), self.cnt[slot:slot + 1].data_ptr(),
+                  net.dn.params.data_ptr(), net.m.data_ptr(), net.v.data_ptr(), counter,
                   net.base.data_ptr(), bc1.data_ptr(), bc2.data_ptr(), net.lr, net.beta1, net.beta2, net.eps,
                   None if target is None else target.params.data_ptr(), self.tau,
                   None if loss is None else loss.data_ptr(), _stream())
@@ -184,6 +189,63 @@ class UpdateEngine:
         self._adam(self.actor, self.ws_a, npa.value, 0, loss=self.aloss)                        # trainer.py:223-225
         _lib.call("cacto_counter_tick", self.cnt[0:1].data_ptr(), st)
 
+    # -- the pipelined schedule (one rank, graphs): the actor update of cycle i needs
+    #    only the critic AFTER update i, so the critic chain runs ahead and keeps each
+    #    cycle's critic in a ring slot (2K slots, written by cycle counter); the actor
+    #    chain reads the slot of its own cycle through a static descriptor (even / odd
+    #    chunks capture their own graphs).  The std phase uses the final critic for all
+    #    M cycles, so its errors v_bar - V(xa) come from ONE batched critic forward.
+    #    Inside a captured chunk cycle i reads counter span[i] (one launch per chunk
+    #    sets span = base + 0..K-1) instead of ticking a counter every cycle.  Same
+    #    kernels on the same inputs: bit-identical to the sequential loop. -----------
+    def _cycle_critic(self, cptr=None):
+        st = _stream()
+        c = self.cnt[0:1].data_ptr() if cptr is None else cptr
+        bd = self._batch(0, cptr=c)
+        npart = ctypes.c_int32(0)
+        tgt = self.target if self.bootstrap else None
+        _lib.call("cacto_critic_loss", self.critic.dn.desc, tgt.desc if tgt else None, bd, self.k_s,
+                  int(self.bootstrap), self.ws_c.data_ptr(), self.ws_c.numel(), npart, st)
+        self._adam(self.critic, self.ws_c, npart.value, 0, target=self.target, loss=self.closs, cptr=c)
+        _lib.call("cacto_ring_copy", self.critic.dn.desc.dtype, self.cring.data_ptr(), c,
+                  self.cring.shape[0], self.cring.shape[1], self.critic.dn.count, self.critic.dn.params.data_ptr(),
+                  1, st)
+        if cptr is None:
+            _lib.call("cacto_counter_tick", c, st)
+
+    def _cycle_actor(self, cptr=None, slot_desc=None):
+        st = _stream()
+        c = self.cnt[2:3].data_ptr() if cptr is None else cptr
+        bd = self._batch(0, cptr=c)
+        if slot_desc is None:  # eager: copy the cycle's critic out of the ring
+            _lib.call("cacto_ring_copy", self.critic.dn.desc.dtype, self.cring.data_ptr(), c,
+                      self.cring.shape[0], self.cring.shape[1], self.critic.dn.count, self.cview.params.data_ptr(),
+                      0, st)
+            slot_desc = self.cview.desc
+        npa = ctypes.c_int32(0)
+        _lib.call("cacto_actor_loss", self.actor.dn.desc, slot_desc, self.sysd, self.costd, bd,
+                  None, self.ws_a.data_ptr(), self.ws_a.numel(), npa, st)
+        self._adam(self.actor, self.ws_a, npa.value, 2, loss=self.aloss, cptr=c)             # trainer.py:223-225
+        if cptr is None:
+            _lib.call("cacto_counter_tick", c, st)
+
+    def _cycle_std_err(self, cptr=None):
+        st = _stream()
+        c = self.cnt[1:2].data_ptr() if cptr is None else cptr
+        bd = self._batch(1, cptr=c)
+        npart = ctypes.c_int32(0)
+        _lib.call("cacto_std_loss_err", self.std.dn.desc, self.serr.data_ptr(), bd, self.ws_s.data_ptr(),
+                  self.ws_s.numel(), npart, st)
+        self._adam(self.std, self.ws_s, npart.value, 1, loss=self.sloss, cptr=c)                # trainer.py:229-232
+        if cptr is None:
+            _lib.call("cacto_counter_tick", c, st)
+
+    def _std_errors(self, M):
+        """e = v_bar - V_critic(xa) of every std-phase minibatch (nets.py:343), one launch."""
+        d = self.buffer.ring_desc(self.idx[1, :M, self.lo:], rows=(self.hi - self.lo))
+        d.rows = M * self.B
+        _lib.call("cacto_value_errors", self.critic.dn.desc, d, self.serr.data_ptr(), _stream())
+
     def _cycle_std(self):
         st = _stream()
         bd = self._batch(1)
@@ -202,31 +264,125 @@ class UpdateEngine:
         self.closs = torch.zeros(M, device=dev, dtype=dt)
         self.aloss = torch.zeros(M, device=dev, dtype=dt)
         self.sloss = torch.zeros(M, device=dev, dtype=dt)
+        self.serr = torch.zeros(M * self.B, device=dev, dtype=dt)   # std-phase errors [M][B]
         self._cap_M = M
         self._graphs = None
 
+    def _pipelined(self):
+        """The pipelined chunk schedule: one rank, graphs on, narrow nets (the std
+        phase's precomputed-error loss is built for hidden width <= 64)."""
+        return self.use_graphs and self.world == 1 and self.std.dn.desc.hp <= 64 and self.critic.dn.desc.hp <= 64
+
     def _capture(self):
-        """Capture one critic+actor cycle and one std cycle.  A first eager pass
-        (on snapshots) performs every lazy runtime set-up outside the capture."""
+        """Capture the cycle graphs (chunks of K cycles for the pipelined schedule,
+        single cycles otherwise).  A first eager pass (on snapshots) performs every
+        lazy runtime set-up outside the capture."""
+        pipe = self._pipelined()
+        dev = device()
+        if pipe and self.cview is None:
+            self.cview = DeviceNet(self.critic.dn.to_mlp(), self.precision)
+            ld = (self.critic.dn.count + 63) // 64 * 64   # 256/512-byte aligned ring slots
+            self.cring = torch.zeros((2 * self.K, ld), device=dev, dtype=torch_dtype(self.precision))
+            # static descriptors of the ring slots (the actor chain's critic of cycle i)
+            self.slot_desc = []
+            for r in range(2 * self.K):
+                d = type(self.cview.desc).from_buffer_copy(self.cview.desc)
+                d.params = self.cring[r].data_ptr()
+                self.slot_desc.append(d)
+            self.span = torch.zeros((3, self.K), device=dev, dtype=torch.int64)
         tensors = [self.actor.dn.params, self.actor.m, self.actor.v, self.critic.dn.params, self.critic.m,
                    self.critic.v, self.std.dn.params, self.std.m, self.std.v, self.target.params, self.cnt]
         saved = [t.clone() for t in tensors]
         self.cnt.zero_()
-        self._cycle_critic_actor()
+        if pipe:
+            self._cycle_critic()
+            self._cycle_actor()
+            self._std_errors(1)
+            self._cycle_std_err()
+        else:
+            self._cycle_critic_actor()
         self._cycle_std()
         torch.cuda.synchronize()
-        for t, s in zip(tensors, saved):
-            t.copy_(s)
-        g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        for t, sv in zip(tensors, saved):
+            t.copy_(sv)
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
+        graphs = {}
+
+        def chunk(fn, which, descs=None):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                _lib.call("cacto_counter_span", self.cnt[which:which + 1].data_ptr(), self.span[which].data_ptr(),
+                          self.K, _stream())
+                for i in range(self.K):
+                    cp = self.span[which, i:i + 1].data_ptr()
+                    if descs is None:
+                        fn(cptr=cp)
+                    else:
+                        fn(cptr=cp, slot_desc=descs[i])
+            return g
+
         with torch.cuda.stream(side):
-            with torch.cuda.graph(g1, stream=side):
-                self._cycle_critic_actor()
-            with torch.cuda.graph(g2, stream=side):
-                self._cycle_std()
+            if pipe:
+                graphs["c"] = chunk(self._cycle_critic, 0)
+                graphs["a0"] = chunk(self._cycle_actor, 2, self.slot_desc[:self.K])
+                graphs["a1"] = chunk(self._cycle_actor, 2, self.slot_desc[self.K:])
+                graphs["s"] = chunk(self._cycle_std_err, 1)
+            else:
+                for name, fn in (("ca", self._cycle_critic_actor), ("s", self._cycle_std)):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=side):
+                        fn()
+                    graphs[name] = g
         torch.cuda.current_stream().wait_stream(side)
-        self._graphs = (g1, g2)
+        self._graphs = graphs
+
+    def _run_pipelined(self, M):
+        """critic chain | actor chain (one chunk of K cycles behind) | std chain (after
+        the last critic chunk), on three streams; the ring holds 2K cycles' critics, so
+        critic chunk j + 2 waits for actor chunk j.  A partial last chunk runs eager."""
+        g = self._graphs
+        K = self.K
+        main = torch.cuda.current_stream()
+        if getattr(self, "_streams", None) is None:
+            self._streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+        sc, sa, ss = self._streams
+        for st in self._streams:
+            st.wait_stream(main)
+        nch = (M + K - 1) // K
+        ev_c = [torch.cuda.Event() for _ in range(nch)]
+        ev_a = [torch.cuda.Event() for _ in range(nch)]
+        for j in range(nch):
+            n = min(K, M - j * K)
+            with torch.cuda.stream(sc):
+                if j >= 2:
+                    sc.wait_event(ev_a[j - 2])
+                if n == K:
+                    g["c"].replay()
+                else:
+                    for _ in range(n):
+                        self._cycle_critic()
+                ev_c[j].record(sc)
+            with torch.cuda.stream(sa):
+                sa.wait_event(ev_c[j])
+                if n == K:
+                    g["a0" if j % 2 == 0 else "a1"].replay()
+                else:
+                    for _ in range(n):
+                        self._cycle_actor()
+                ev_a[j].record(sa)
+        with torch.cuda.stream(ss):
+            ss.wait_event(ev_c[nch - 1])
+            self._std_errors(M)
+            for j in range(nch):
+                n = min(K, M - j * K)
+                if n == K:
+                    g["s"].replay()
+                else:
+                    for _ in range(n):
+                        self._cycle_std_err()
+        main.wait_stream(sa)
+        main.wait_stream(ss)
 
     # -- the update loop ----------------------------------------------------------------
     def run(self, m_updates: int, rng: np.random.Generator):
@@ -249,12 +405,13 @@ class UpdateEngine:
         if self.use_graphs and self._graphs is None:
             self._capture()
         self.cnt.zero_()
-        if self.use_graphs:
-            g1, g2 = self._graphs
+        if self._pipelined():
+            self._run_pipelined(M)
+        elif self.use_graphs:
             for _ in range(M):
-                g1.replay()
+                self._graphs["ca"].replay()
             for _ in range(M):
-                g2.replay()
+                self._graphs["s"].replay()
         else:
             for _ in range(M):
                 self._cycle_critic_actor()

@@ -188,3 +188,33 @@ def test_training_state_resume_is_bitwise(graphs, tmp_path):
         assert eng2.critic.step == eng.critic.step
     finally:
         P.set_precision(old)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_pipelined_update_loop_is_bitwise_the_sequential_one(prec):
+    """The graph schedule runs the critic chain ahead of the actor chain (each actor
+    update reads a ring copy of the critic of its own cycle) and the std chain beside
+    the actor chain's tail: same kernels on the same inputs, so the losses and every
+    parameter equal the plain sequential loop bit for bit (M = 37: two full 16-cycle
+    chunks, a partial one, and a ring wrap)."""
+    from dp_setup import engine_setup
+    old = P.get_precision()
+    P.set_precision(prec)
+    try:
+        res = []
+        for graphs in (False, True):
+            eng, seed = engine_setup(64)
+            eng.use_graphs = graphs
+            rng = np.random.default_rng(seed)
+            c1, s1 = eng.run(37, rng)
+            c2, s2 = eng.run(5, rng)           # a second run continues the streams
+            res.append((c1, s1, c2, s2, [np.asarray(p) for n in eng.networks() for p in n.flat_params()],
+                        eng.actor.step))
+        a, b = res
+        for x, y in zip(a[:4], b[:4]):
+            np.testing.assert_array_equal(x, y)
+        for x, y in zip(a[4], b[4]):
+            np.testing.assert_array_equal(x, y)
+        assert a[5] == b[5] == 42
+    finally:
+        P.set_precision(old)
