@@ -203,13 +203,25 @@ extern "C" int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost
 }
 
 namespace cacto {
+// a block takes 8 kept columns: their indices loaded once, then every thread copies
+// rows r = tid, tid + blockDim, ... of all 8 (8 independent scattered loads in flight
+// per thread, coalesced stores along r); 32-bit row arithmetic
 template <typename T>
-__global__ void take_columns_kernel(const T* __restrict__ src, int64_t R, int64_t N, const int64_t* __restrict__ idx,
-                                    int64_t K, T* dst) {
-  const int64_t total = R * K;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / R, rr = e - i * R;
-    dst[e] = src[rr * N + idx[i]];
+__global__ void __launch_bounds__(128) take_columns_kernel(const T* __restrict__ src, int64_t R, int64_t N,
+                                                           const int64_t* __restrict__ idx, int64_t K, T* dst) {
+  const int64_t i0 = (int64_t)blockIdx.x * 8;
+  int64_t col[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) col[u] = i0 + u < K ? idx[i0 + u] : -1;
+  const int r_n = (int)R;
+  for (int r = threadIdx.x; r < r_n; r += blockDim.x) {
+    const T* row = src + (int64_t)r * N;
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = col[u] >= 0 ? __ldg(row + col[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (col[u] >= 0) dst[(i0 + u) * R + r] = v[u];
   }
 }
 // dst[i, :] = src[idx[i], :] for rows of R elements: one warp per row, 16-byte
@@ -252,12 +264,12 @@ extern "C" int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int
   if (R < 0 || N < 0 || K < 0 || (R * K > 0 && (!src || !idx || !dst)))
     return set_error(CACTO_EVALUE, "take_columns: bad arguments");
   if (R * K == 0) return CACTO_OK;
-  const int64_t total = R * K;
-  unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 16 * (int64_t)num_sms());
+  if (R > 0x7fffffff || (K + 7) / 8 > 0x7fffffff) return set_error(CACTO_EVALUE, "take_columns: too large");
+  const unsigned grid = (unsigned)((K + 7) / 8);
   if (dtype == CACTO_F32)
-    take_columns_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)src, R, N, idx, K, (float*)dst);
+    take_columns_kernel<float><<<grid, 128, 0, (cudaStream_t)stream>>>((const float*)src, R, N, idx, K, (float*)dst);
   else
-    take_columns_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)src, R, N, idx, K,
+    take_columns_kernel<double><<<grid, 128, 0, (cudaStream_t)stream>>>((const double*)src, R, N, idx, K,
                                                                          (double*)dst);
   return check_launch("take_columns_kernel");
 }
