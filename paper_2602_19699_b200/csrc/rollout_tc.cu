@@ -187,7 +187,13 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       if (lane == 0) tc::mbar_arrive(&full_bar[g]);
     };
     auto wait_done = [&]() {
-#ifdef CACTO_RTC_PLAIN_WAIT
+#ifndef CACTO_RTC_POLL_ALL
+      // one warp of the tile polls the MMA barrier; the tile's other epilogue warps
+      // block in a named barrier (no polling instructions on their schedulers):
+      // manipulator3 K1 3.84 -> 3.78 ms (profiles/README.md)
+      if ((warp % WPT) == 0) tc::mbar_wait_sleep(&done_bar[g], pd);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(WPT * 32) : "memory");
+#elif defined(CACTO_RTC_PLAIN_WAIT)
       tc::mbar_wait(&done_bar[g], pd);
 #else
       tc::mbar_wait_sleep(&done_bar[g], pd);
