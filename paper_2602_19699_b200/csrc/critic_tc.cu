@@ -813,7 +813,6 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
   const uint32_t tmem = tmem_sh;
   const uint32_t sb = saddr(base);
   unsigned char* raw = base + WG_STAGES * WG_STAGE;
-  const uint32_t rsb = saddr(raw);
 
   if (warp == WG_TMA_WARP) {
     if (lane == 0) {
@@ -837,21 +836,25 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
     for (int kb = 0; kb < nkb; ++kb) {
       const int rs = kb % WG_RAW, s = kb % WG_STAGES;
       tc::mbar_wait(&raw_full[rs], (kb / WG_RAW) & 1);
+      // k-blocks never straddle a chunk end (chunks are multiples of 64 samples) and rows
+      // past K2 are TMA zero fill: no per-row masks
       float v[3][8];
-      const uint32_t rb = rsb + (uint32_t)rs * WG_RSTAGE;
-      const int64_t b0 = k0 + (int64_t)kb * WG_KB + sg * 8;
+      const float* rp = reinterpret_cast<const float*>(raw + (uint32_t)rs * WG_RSTAGE) + sg * 8 * 64;
+      if (gw) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const bool ok = b0 + j < k1;  // rows past K2 are TMA zero fill; past k1 belong to the next CTA
-        const int sj = sg * 8 + j;
-        if (gw) {
-          v[0][j] = ok ? lds1f(rb + (uint32_t)(sj * 64 + lane) * 4) : 0.f;
-          v[1][j] = ok ? lds1f(rb + (uint32_t)(sj * 64 + lane + 32) * 4) : 0.f;
-        } else {
+        for (int j = 0; j < 8; ++j) {
+          v[0][j] = rp[j * 64 + lane];
+          v[1][j] = rp[j * 64 + lane + 32];
+        }
+      } else {
+        const float* up = reinterpret_cast<const float*>(raw + (uint32_t)rs * WG_RSTAGE + WG_RG) + sg * 8 * uw;
 #pragma unroll
-          for (int rr = 0; rr < 3; ++rr) {
-            const int c = lane + 32 * rr;
-            v[rr][j] = (ok && c < ncol) ? lds1f(rb + WG_RG + (uint32_t)(sj * uw + c) * 4) : 0.f;
+        for (int rr = 0; rr < 3; ++rr) {
+          const int c = lane + 32 * rr;
+          if (32 * rr < ncol) {  // warp-uniform
+            const int cc = c < ncol ? c : 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[rr][j] = up[j * uw + cc];
           }
         }
       }
@@ -872,11 +875,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
 #pragma unroll
         for (int rr = 0; rr < 3; ++rr) {
           const int c = lane + 32 * rr;
-          if (c < ncol) {
+          if (32 * rr < ncol) {  // warp-uniform; lanes past ncol skip the store only
             split8(v[rr], hi, lo);
             const uint32_t off = (uint32_t)c * 128 + (uint32_t)((sg ^ (c & 7)) << 4);
-            sts128(st0 + WG_A + off, hi);
-            sts128(st0 + WG_A + WG_B + off, lo);
+            if (c < ncol) {
+              sts128(st0 + WG_A + off, hi);
+              sts128(st0 + WG_A + WG_B + off, lo);
+            }
           }
         }
       }
