@@ -169,6 +169,7 @@ struct CriticArgs {
   T k_s;
   const T* v_next;  // [rows] target value at x_{+k} (bootstrap) or null
   T* ws;            // [grid][P+1]
+  int smem_slot;    // accumulate the CTA's gradient slot in shared memory, store it once
 };
 
 template <typename T, int HP, int IP, int S>
@@ -194,10 +195,14 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
   T* EV = p;  // [S] target y, then e_v, then delta
   p += S;
   T* EG = p;  // [n][S] gradient errors
+  p += (size_t)CACTO_MAX_IN * S;
 
   net.stage(a.params);
   const int64_t P_total = a.off.total;
-  T* slot = a.ws + (int64_t)blockIdx.x * (P_total + 1);
+  T* const gslot = a.ws + (int64_t)blockIdx.x * (P_total + 1);
+  // the CTA's gradient slot: in shared memory when it fits (one coalesced store at
+  // the end instead of read-modify-writes through L2 per tile), else in the workspace
+  T* slot = a.smem_slot ? p : gslot;
   zero_slot(slot, P_total + 1);
 
   const TL tl;
@@ -333,6 +338,8 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
     }
     __syncthreads();
   }
+  if (a.smem_slot)
+    for (int64_t i = threadIdx.x; i <= P_total; i += kThreads) gslot[i] = slot[i];
 }
 
 // =====================================================================================
@@ -361,6 +368,7 @@ struct VpArgs {
   const T* vn;      // [rows] critic value at xn
   const T* gn;      // [rows][n+1] critic state gradient at xn
   T* ws;
+  int smem_slot;    // accumulate the CTA's gradient slot in shared memory, store it once
 };
 
 enum { VP_STD = 0, VP_ACTOR = 1 };
@@ -388,7 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
 
   net.stage(a.params);
   const int64_t P_total = a.off.total;
-  T* slot = a.ws + (int64_t)blockIdx.x * (P_total + 1);
+  T* const gslot = a.ws + (int64_t)blockIdx.x * (P_total + 1);
+  T* slot = a.smem_slot ? p : gslot;  // as critic_kernel
   zero_slot(slot, P_total + 1);
   T inv_denom = a.live_rows ? T(1) / (T)(*a.live_rows) : a.inv_denom;
   if (a.count_live) {  // rows with t < t_max (nets.py:310-312), counted by every CTA
@@ -498,6 +507,8 @@ __global__ void __launch_bounds__(kThreads, 1) vp_kernel(const VpArgs<T> a) {
     }
     __syncthreads();
   }
+  if (a.smem_slot)
+    for (int64_t i = threadIdx.x; i <= P_total; i += kThreads) gslot[i] = slot[i];
 }
 
 // ---- actor prep: actor forward + stage cost + dynamics -> x' (nets.py:319-325) -----
@@ -599,6 +610,21 @@ int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_bat
 int cacto_forward_rows(const cacto_mlp_t* mlp, const cacto_batch_t* rows_of, int which, void* out,
                        void* stream);  // forward.cu helper (gathered rows)
 
+// the gradient slot goes to shared memory when the kernel's tiles + slot fit the
+// per-CTA limit (CACTO_SMEM_SLOT=0 keeps it in the workspace: A/B measurements)
+static int smem_slot_fits(const void* kern, size_t bytes) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("CACTO_SMEM_SLOT");
+    env = e ? atoi(e) : 1;
+  }
+  int dev = 0, maxb = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxb, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  (void)kern;
+  return env != 0 && bytes + 1024 <= (size_t)maxb;
+}
+
 static int loss_grid(int64_t rows, int S) {
   int64_t tiles = (rows + S - 1) / S;
   int64_t cap = num_sms();
@@ -640,10 +666,14 @@ static int launch_critic_s(const CriticArgs<T>& a, int64_t rows, int* grid_out, 
               (size_t)CACTO_MAX_IN * S;
   size_t bytes = el * sizeof(T);
   auto kern = critic_kernel<T, HP, IP, S>;
+  CriticArgs<T> b = a;
+  const size_t slot_bytes = ((size_t)a.off.total + 1 + 3) / 4 * 4 * sizeof(T);
+  b.smem_slot = smem_slot_fits((const void*)kern, bytes + slot_bytes);
+  if (b.smem_slot) bytes += slot_bytes;
   if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_EUNSUPPORTED, "critic_loss: %zu B shared memory not available", bytes);
   int grid = loss_grid(rows, S);
-  kern<<<grid, kThreads, bytes, st>>>(a);
+  kern<<<grid, kThreads, bytes, st>>>(b);
   *grid_out = grid;
   return check_launch("critic_kernel");
 }
@@ -724,10 +754,14 @@ static int launch_vp_s(const VpArgs<T>& a, int64_t rows, int* grid_out, cudaStre
               (size_t)CACTO_MAX_OUT * S + 4 * ((CACTO_MAX_OUT + 3) / 4) * S;
   size_t bytes = el * sizeof(T);
   auto kern = vp_kernel<T, HP, IP, S, KIND, SYS>;
+  VpArgs<T> b = a;
+  const size_t slot_bytes = ((size_t)a.off.total + 1 + 3) / 4 * 4 * sizeof(T);
+  b.smem_slot = smem_slot_fits((const void*)kern, bytes + slot_bytes);
+  if (b.smem_slot) bytes += slot_bytes;
   if (!ensure_smem((const void*)kern, bytes))
     return set_error(CACTO_EUNSUPPORTED, "loss: %zu B shared memory not available", bytes);
   int grid = loss_grid(rows, S);
-  kern<<<grid, kThreads, bytes, st>>>(a);
+  kern<<<grid, kThreads, bytes, st>>>(b);
   *grid_out = grid;
   return check_launch("vp_kernel");
 }
