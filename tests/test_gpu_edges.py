@@ -12,6 +12,7 @@
 """
 
 import numpy as np
+from pathlib import Path
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -218,3 +219,98 @@ def test_pipelined_update_loop_is_bitwise_the_sequential_one(prec):
         assert a[5] == b[5] == 42
     finally:
         P.set_precision(old)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_std_loss_from_precomputed_errors_is_bitwise(prec):
+    """cacto_value_errors + cacto_std_loss_err (the update loop's std phase) equal
+    cacto_std_loss (critic forward inside) bit for bit, cycle by cycle."""
+    import ctypes
+    from paper_2602_19699_b200.device import DeviceNet, torch_dtype
+    from dp_setup import engine_setup
+    old = P.get_precision()
+    P.set_precision(prec)
+    try:
+        eng, seed = engine_setup(64)
+        M, B = 5, 64
+        rng = np.random.default_rng(seed)
+        lists = np.stack([eng.buffer.draw_indices(B, rng) for _ in range(M)])
+        idx = torch.as_tensor(lists).cuda()
+        cnt = torch.zeros(1, device="cuda", dtype=torch.int64)
+        st = torch.cuda.current_stream().cuda_stream
+        ws = torch.empty(_lib.load().cacto_loss_workspace_bytes(eng.std.dn.desc, B), device="cuda", dtype=torch.uint8)
+        dall = eng.buffer.ring_desc(idx, rows=M * B)
+        err = torch.empty(M * B, device="cuda", dtype=torch_dtype(prec))
+        _lib.call("cacto_value_errors", eng.critic.dn.desc, dall, err.data_ptr(), st)
+        for c in range(M):
+            cnt.fill_(c)
+            d = eng.buffer.ring_desc(idx, rows=B)
+            d.cycle = cnt.data_ptr()
+            d.idx_stride = B
+            g = []
+            for fn, args in (("cacto_std_loss", (eng.std.dn.desc, eng.critic.dn.desc, d)),
+                             ("cacto_std_loss_err", (eng.std.dn.desc, err.data_ptr(), d))):
+                npart = ctypes.c_int32(0)
+                _lib.call(fn, *args, ws.data_ptr(), ws.numel(), npart, st)
+                out = torch.empty(eng.std.dn.count + 1, device="cuda", dtype=torch_dtype(prec))
+                _lib.call("cacto_reduce_grads", eng.std.dn.desc.dtype, ws.data_ptr(), npart.value, eng.std.dn.count,
+                          out.data_ptr(), out[eng.std.dn.count:].data_ptr(), st)
+                g.append(out.cpu().numpy())
+            np.testing.assert_array_equal(g[0], g[1])
+    finally:
+        P.set_precision(old)
+
+
+def test_critic_wgrad_reduction_matches_gemm_path():
+    """The fp16-pair tensor-core weight-gradient reduction (default) and the 3xTF32 GEMM
+    reductions (CACTO_CRITIC_WGRAD=0) agree to fp32 accuracy, and both match the
+    float64 oracle within the SURVEY 8(c) bounds (loss 1e-5, grads 1e-4 of max|g|)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+import paper_2602_19699_b200 as P
+from paper_2602_19699_b200 import nets as B_nets, specs as B_specs
+from oracle import nets as O_nets
+from types import SimpleNamespace
+P.set_precision('fp32')
+spec, fld = B_specs.config('manipulator3')
+rng = np.random.default_rng(21)
+c, h = B_specs.normalisation(spec)
+critic = B_nets.init_mlp([7, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+target = B_nets.init_mlp([7, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+B = 20000
+lo, hi = B_specs.region_box(spec)
+xa = np.concatenate([rng.uniform(size=(B, 6)) * (hi - lo) + lo, rng.integers(0, 100, (B, 1))], 1)
+xk = np.concatenate([rng.uniform(size=(B, 6)) * (hi - lo) + lo, rng.integers(1, 101, (B, 1))], 1)
+b = SimpleNamespace(xa=xa, u=rng.normal(size=(B, 3)), v_bar=rng.normal(size=B) * 30, v_bar_x=rng.normal(size=(B, 6)),
+                    xa_plus_k=xk, t_max=100)
+loss, g = B_nets.critic_loss(critic, target, b, 0.7, True)
+np.savez(sys.argv[1], loss=loss, *g)
+"""
+    outs = []
+    for v in ("1", "0"):
+        path = f"/tmp/wgrad_{v}.npz"
+        env = dict(os.environ, CACTO_CRITIC_WGRAD=v)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, cwd=str(Path(__file__).parents[1]))
+        outs.append(np.load(path))
+    from types import SimpleNamespace
+    spec, fld = B_specs.config("manipulator3")
+    rng = np.random.default_rng(21)
+    c, h = B_specs.normalisation(spec)
+    critic = B_nets.init_mlp([7, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+    target = B_nets.init_mlp([7, 64, 64, 64, 1], rng, in_center=c, in_half=h)
+    B = 20000
+    lo, hi = B_specs.region_box(spec)
+    xa = np.concatenate([rng.uniform(size=(B, 6)) * (hi - lo) + lo, rng.integers(0, 100, (B, 1))], 1)
+    xk = np.concatenate([rng.uniform(size=(B, 6)) * (hi - lo) + lo, rng.integers(1, 101, (B, 1))], 1)
+    b = SimpleNamespace(xa=xa, u=rng.normal(size=(B, 3)), v_bar=rng.normal(size=B) * 30,
+                        v_bar_x=rng.normal(size=(B, 6)), xa_plus_k=xk, t_max=100)
+    ref_loss, ref_g = O_nets.critic_loss(critic, target, b, 0.7, True)
+    scale = max(np.abs(r).max() for r in ref_g)
+    for o in outs:
+        assert abs(float(o["loss"]) - ref_loss) <= 1e-5 * abs(ref_loss)
+        for i, r in enumerate(ref_g):
+            assert np.abs(o[f"arr_{i}"] - r).max() <= 1e-4 * scale, i
