@@ -360,6 +360,16 @@ def ncu_traffic(kernel_prefix, workload):
         return None
 
 
+def _max_over_ranks(v: float) -> float:
+    """Device-side MAX over ranks (NCCL; a host tensor under the gloo test backend)."""
+    import torch
+    import torch.distributed as dist
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([v], device="cuda" if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def reference_arm(args, spec, field, actor, critic, std, T, rank):
     if rank != 0:
         return
@@ -420,9 +430,16 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # CACTO_BENCH_BACKEND=gloo (tests only): the N > 1 code path on ONE GPU, every rank
+    # on cuda:(local_rank % device_count), collectives through gloo
+    backend = os.environ.get("CACTO_BENCH_BACKEND", "nccl")
+    local_dev = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    torch.cuda.set_device(local_rank)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_dev))
+        else:
+            dist.init_process_group(backend)
+    torch.cuda.set_device(local_dev)
     import paper_2602_19699_b200 as P
     from paper_2602_19699_b200 import _lib, parallel, trainer
     P.set_precision(args.precision)
@@ -468,13 +485,11 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-            t = torch.tensor([total], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total = float(t.item())
+            total = _max_over_ranks(total)
         return total / K  # ms per step
 
     # ---- device-resident value ----------------------------------------------------
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(local_dev)
     for _ in range(args.warmup):
         step(x0_dev)
     clocks.start()
@@ -681,7 +696,8 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None, H=HIDDEN
         else:
             _lib.call("cacto_reduce_grads", net.desc.dtype, ws.data_ptr(), npart.value, net.count, g.data_ptr(),
                       g[net.count:].data_ptr(), stream)
-            dist.all_reduce(g)
+            from paper_2602_19699_b200.parallel import all_reduce_sum
+            all_reduce_sum(g)
             _lib.call("cacto_adam_step", net.desc.dtype, net.params.data_ptr(), m.data_ptr(), v.data_ptr(),
                       g.data_ptr(), net.count, step_no[0], 1e-3, 0.9, 0.999, 1e-8, stream)
             _lib.call("cacto_polyak", net.desc.dtype, tgt.params.data_ptr(), net.params.data_ptr(), net.count, 0.005,
@@ -701,9 +717,7 @@ def critic_bench(torch, P, stream, B=65536, world=1, rank=0, dist=None, H=HIDDEN
     b.synchronize()
     ms = a.elapsed_time(b) / K
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks(ms)
     d = spec.n + 1
     f = 28 * H * H + 14 * d * H + 8 * H
     peak, peak_source = tensor_peak()
