@@ -9,7 +9,8 @@ actor rollout with running + terminal cost (K1), critic V(x0) and std sigma(x0)
 (K2, fused into the K1 launch), score sigma*|V - J|, a stable top-(N/10) select
 (K3), and the kept 1/10's warm starts U (taken from the K1 controls).  `value` is device-resident
 (inputs already in HBM); `e2e` goes through the public API with the candidate
-states in pinned host memory and the kept indices + warm starts read back.
+states in pinned host memory (read zero-copy by the rollout kernel) and the kept
+indices + warm starts returned to pinned host memory.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -51,6 +52,10 @@ WORKLOADS = {"dubins": 65536, "pointmass": 750, "manipulator3": 262144, "aliengo
 HIDDEN = 64
 CAND_MULT = 10
 SEED = 0
+# e2e: warm starts written zero-copy into pinned host memory by the take kernel (1) or
+# taken on the device and copied by the copy engine (0, measured faster: the 31.5 MB
+# of manipulator3 warm starts stream at full PCIe rate from a copy, not from SM stores)
+E2E_ZC_U = os.environ.get("CACTO_E2E_ZC_U", "0") == "1"
 
 
 # ---------------------------------------------------------------------------------
@@ -506,11 +511,18 @@ def main():
     d2h_rows = [0]
 
     def e2e_step():
-        xd = x0_pinned.to("cuda", non_blocking=True)
-        order, U = step(xd)
-        order_host.copy_(order, non_blocking=True)
-        k = U.shape[0]
-        U_host[:k].copy_(U, non_blocking=True)
+        # the public call with HOST buffers: the rollout kernel reads the pinned x0
+        # zero-copy and the take kernel writes the warm starts into pinned U_host
+        # (both transfers cross PCIe inside the step, overlapped with the kernels)
+        uo = U_host if E2E_ZC_U else None
+        if world == 1:
+            out = pipe.run(x0_pinned, keep_global, u_out=uo)
+        else:
+            out = pipe.run_sharded(x0_pinned, keep_global, base, dsel=dsel, u_out=uo)
+        order_host.copy_(out["order"], non_blocking=True)
+        k = out["U"].shape[0]
+        if uo is None:
+            U_host[:k].copy_(out["U"], non_blocking=True)
         d2h_rows[0] = k
 
     e2e_ms = timed(e2e_step, args.steps, args.warmup)

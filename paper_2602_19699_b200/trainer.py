@@ -31,6 +31,12 @@ import os
 _TMAJOR = os.environ.get("CACTO_WARM_TMAJOR", "1") == "1"
 
 
+def _dev(x0: torch.Tensor) -> torch.device:
+    """Where the step's buffers live: x0's device, or the current GPU when x0 is a
+    pinned host tensor (read zero-copy by the rollout kernel over PCIe/UVA)."""
+    return torch.device("cuda", torch.cuda.current_device()) if x0.device.type == "cpu" else x0.device
+
+
 def _stream():
     return torch.cuda.current_stream().cuda_stream
 
@@ -153,11 +159,11 @@ class BicPipeline:
         kept warm starts are taken (no second rollout)."""
         N = x0.shape[0]
         dt = torch_dtype(self.precision)
-        cost = torch.empty(N, device=x0.device, dtype=dt)
+        cost = torch.empty(N, device=_dev(x0), dtype=dt)
         T = self.model.t_max - t0
         U, flags = None, 0
         if keep_controls:
-            U, flags = self._u_all(N, T, dt, x0.device)
+            U, flags = self._u_all(N, T, dt, _dev(x0))
         _lib.call("cacto_rollout_ex", self.sysd, self.costd, self.actor.desc, x0.data_ptr(), None, t0, N, T, flags,
                   U, None, None, cost.data_ptr(), _stream())
         return cost
@@ -167,12 +173,12 @@ class BicPipeline:
         library reports the nets are not fusable."""
         N = x0.shape[0]
         dt = torch_dtype(self.precision)
-        cost = torch.empty(N, device=x0.device, dtype=dt)
-        scores = torch.empty(N, device=x0.device, dtype=dt)
+        cost = torch.empty(N, device=_dev(x0), dtype=dt)
+        scores = torch.empty(N, device=_dev(x0), dtype=dt)
         T = self.model.t_max - t0
         U, flags = None, 0
         if keep_controls:
-            U, flags = self._u_all(N, T, dt, x0.device)
+            U, flags = self._u_all(N, T, dt, _dev(x0))
         rc = _lib.load().cacto_rollout_score(
             self.sysd, self.costd, self.actor.desc, _lib.SCORE[self.mode], self.std.desc if self.std else None,
             self.critic.desc if self.critic else None, x0.data_ptr(), t0, N, T, flags, U, cost.data_ptr(),
@@ -195,19 +201,27 @@ class BicPipeline:
             if scores is None:  # not fusable (fp64 / SIMT path / differing net shapes)
                 cost = self.rollout_costs(x0, t0, keep_controls=reuse)
         if scores is None:
-            xa = torch.empty((N, n + 1), device=x0.device, dtype=dt)
+            xa = torch.empty((N, n + 1), device=_dev(x0), dtype=dt)
             xa[:, :n] = x0
             xa[:, n] = float(t0)
             launches += 3  # torch copy + fill of the augmented view, K2 score
             scores = score_device(self.mode, xa, self.std, self.critic, cost)
         return scores, cost, launches
 
-    def _warm(self, x0: torch.Tensor, sel: torch.Tensor, t0: int, reuse: bool):
-        """Warm starts U [K, T, m] of the candidates `sel` (local indices)."""
+    def _warm(self, x0: torch.Tensor, sel: torch.Tensor, t0: int, reuse: bool, out=None):
+        """Warm starts U [K, T, m] of the candidates `sel` (local indices).  `out`
+        (pinned host [>= K, T, m]) makes the take write them straight into host memory
+        (zero-copy over PCIe/UVA: the gather and the transfer overlap)."""
         N = x0.shape[0]
         K = sel.shape[0]
         T = self.model.t_max - t0
-        U = torch.empty((K, T, self.model.m), device=x0.device, dtype=torch_dtype(self.precision))
+        dt = torch_dtype(self.precision)
+        if out is not None and reuse:
+            U = out[:K]
+            if U.dtype != dt or tuple(U.shape[1:]) != (T, self.model.m) or not U.is_contiguous():
+                raise ValueError("warm-start output buffer does not match [K, T, m] / dtype")
+        else:
+            U = torch.empty((K, T, self.model.m), device=_dev(x0), dtype=dt)
         if K == 0:
             return U, 0
         if reuse:
@@ -220,13 +234,21 @@ class BicPipeline:
                 _lib.call("cacto_take_rows", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
                           sel.data_ptr(), K, U.data_ptr(), _stream())
             return U, 1
-        kept = x0.index_select(0, sel)
+        kept = x0.to(_dev(x0)).index_select(0, sel)
         _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, K, T,
                   U.data_ptr(), None, None, None, _stream())
+        if out is not None:
+            out[:K].copy_(U, non_blocking=True)
+            U = out[:K]
         return U, 2
 
-    def run(self, x0: torch.Tensor, keep: int, t0: int = 0, warm_starts: bool = True):
-        """x0 float64 [N, n] on device -> dict(order, scores, U, cost)."""
+    def run(self, x0: torch.Tensor, keep: int, t0: int = 0, warm_starts: bool = True, u_out=None):
+        """x0 float64 [N, n] on device -> dict(order, scores, U, cost).
+
+        x0 may also be a PINNED HOST tensor: the rollout kernel then reads each start
+        zero-copy (over PCIe / UVA, overlapped with the other CTAs' compute) instead of
+        a separate host-to-device copy; `u_out` (pinned host [>= keep, T, m]) receives
+        the warm starts straight from the take kernel (trainer.py:192-193 hand-off)."""
         N, n = x0.shape
         reuse = warm_starts and keep > 0 and self.mode != "std"
         scores, cost, launches = self._scores(x0, t0, reuse)
@@ -237,7 +259,7 @@ class BicPipeline:
             launches += 4 + max(0, int(np.ceil(np.log2(max(keep, 1) / 2048.0))))  # memset, select, sort, merges, emit
         out = {"order": order, "scores": top, "cost": cost}
         if warm_starts and keep > 0:
-            out["U"], nl = self._warm(x0, order, t0, reuse)
+            out["U"], nl = self._warm(x0, order, t0, reuse, out=u_out)
             launches += nl
         if self.base_index:
             out["order"] = order + self.base_index
@@ -245,7 +267,7 @@ class BicPipeline:
         return out
 
     def run_sharded(self, x0: torch.Tensor, keep_global: int, base_index: int, dsel=None, group=None,
-                    t0: int = 0, warm_starts: bool = True):
+                    t0: int = 0, warm_starts: bool = True, u_out=None):
         """This rank's share of the multi-GPU rollout+BIC step.
 
         x0 [N_local, n] are global candidates base_index .. base_index + N_local - 1
@@ -260,13 +282,13 @@ class BicPipeline:
         reuse = warm_starts and keep_global > 0 and self.mode != "std"
         scores, cost, launches = self._scores(x0, t0, reuse)
         if dsel is None:
-            dsel = DistributedSelect(N, keep_global, scores.dtype, group, x0.device)
+            dsel = DistributedSelect(N, keep_global, scores.dtype, group, _dev(x0))
         order, top, local, _ = dsel.run(scores, base_index)
         # hist + digit per pass; compact, chunk sort, merges, emit; final chunk sort, merges, emit
         launches += 2 * dsel.passes + 5 + 2 * max(0, int(np.ceil(np.log2(max(keep_global, 1) / 2048.0))))
         out = {"order": order, "scores": top, "cost": cost, "local": local}
         if warm_starts:
-            out["U"], nl = self._warm(x0, local, t0, reuse)
+            out["U"], nl = self._warm(x0, local, t0, reuse, out=u_out)
             launches += nl
         self.kernel_launches = launches
         return out

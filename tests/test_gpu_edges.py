@@ -314,3 +314,28 @@ np.savez(sys.argv[1], loss=loss, *g)
         assert abs(float(o["loss"]) - ref_loss) <= 1e-5 * abs(ref_loss)
         for i, r in enumerate(ref_g):
             assert np.abs(o[f"arr_{i}"] - r).max() <= 1e-4 * scale, i
+
+
+def test_bic_pipeline_host_buffers_zero_copy():
+    """BicPipeline.run with a pinned HOST x0 (read zero-copy by the rollout kernel) and
+    a pinned host warm-start buffer (written by the take kernel) gives exactly the
+    device-resident results."""
+    from bench import make_nets, candidates
+    old = P.get_precision()
+    P.set_precision("fp32")
+    try:
+        spec, fld = B_specs.config("dubins")
+        actor, critic, std = make_nets(spec)
+        N, keep = 20000, 2000
+        x0h = torch.from_numpy(candidates(spec, 0, N)).pin_memory()
+        pipe = B_trainer.BicPipeline(spec, fld, actor, critic, std, mode="std_x_gap")
+        ref = pipe.run(x0h.cuda(), keep)
+        Uh = torch.empty((keep, spec.t_max, spec.m), dtype=torch.float32).pin_memory()
+        got = pipe.run(x0h, keep, u_out=Uh)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got["order"].cpu().numpy(), ref["order"].cpu().numpy())
+        np.testing.assert_array_equal(got["scores"].cpu().numpy(), ref["scores"].cpu().numpy())
+        np.testing.assert_array_equal(Uh.numpy(), ref["U"].cpu().numpy())
+        assert got["U"].data_ptr() == Uh.data_ptr()
+    finally:
+        P.set_precision(old)
