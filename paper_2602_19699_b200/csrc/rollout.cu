@@ -94,12 +94,10 @@ rollout_kernel(const RolloutArgs<T> a) {
 #pragma unroll
         for (int j = 0; j < m; ++j) a.U[a.u_at(gi, k, j, m)] = u[j];
       }
-      T sc = T(0);
-      if (a.has_cost) sc = stage_cost<SYS>(a.sys, a.cost, x, u);
+      T xn[n];
+      const T sc = cost_and_step<SYS>(a.sys, a.cost, a.has_cost, x, u, xn);
       acc.add(k, sc);
       if (a.SC) a.SC[gi * (int64_t)(a.t_stride + 1) + k] = sc;
-      T xn[n];
-      step<SYS>(a.sys, x, u, xn);
 #pragma unroll
       for (int c = 0; c < n; ++c) x[c] = xn[c];
       if (a.X) {

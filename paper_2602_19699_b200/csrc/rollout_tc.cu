@@ -261,12 +261,10 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
 #pragma unroll
             for (int j = 0; j < m; ++j) a.U[a.u_at(gi, k, j, m)] = u[j];
           }
-          float sc = 0.f;
-          if (a.has_cost) sc = stage_cost<SYS>(a.sys, a.cost, x, u);
+          float xn[n];
+          const float sc = cost_and_step<SYS>(a.sys, a.cost, a.has_cost, x, u, xn);
           acc.add(k, sc);
           if (a.SC) a.SC[gi * (int64_t)(a.t_stride + 1) + k] = sc;
-          float xn[n];
-          step<SYS>(a.sys, x, u, xn);
 #pragma unroll
           for (int c = 0; c < n; ++c) x[c] = xn[c];
           if (a.X) {

@@ -108,11 +108,19 @@ template <> struct SysDims<CACTO_SYS_ALIENGO_LIPM> { static constexpr int n = 15
 // symmetric M(q) entries and the Coriolis vector h(q, dq), manipulator.py:51-84:
 // h = sum_k dq_k dM_k dq - 0.5 [dq^T dM_i dq]_i  (c_ijk Christoffel identity)
 template <typename T>
+CACTO_D void manip_mass_trig(const SysDev<T>& P, const T* dq, T s2, T c2, T s3, T c3, T s23, T c23, T M[6],
+                             T h[3]);
+template <typename T>
 CACTO_D void manip_mass(const SysDev<T>& P, const T* q, const T* dq, T M[6], T h[3]) {
   T s2, c2, s3, c3, s23, c23;
   m_sincos(q[1], &s2, &c2);
   m_sincos(q[2], &s3, &c3);
   m_sincos(q[1] + q[2], &s23, &c23);
+  manip_mass_trig(P, dq, s2, c2, s3, c3, s23, c23, M, h);
+}
+template <typename T>
+CACTO_D void manip_mass_trig(const SysDev<T>& P, const T* dq, T s2, T c2, T s3, T c3, T s23, T c23, T M[6],
+                             T h[3]) {
   // M = A0 + c2 B12 + c23 B13 + c3 B23 -> (00, 01, 02, 11, 12, 22)
   M[0] = P.a0_00 + T(2) * P.b12 * c2 + T(2) * P.b13 * c23 + T(2) * P.b23 * c3;
   M[1] = P.a0_01 + P.b12 * c2 + P.b13 * c23 + T(2) * P.b23 * c3;
@@ -338,6 +346,54 @@ CACTO_D T terminal_cost(const SysDev<T>& P, const CostDev<T>& C, const T* x) {
     T px, py;
     task_point<SYS>(P, x, px, py);
     return point_value(C, px, py);
+  }
+}
+
+// stage cost l(x, u) then the Euler step x' = f(x, u) at the same x (the rollout
+// and actor-loss epilogues).  fp32 manipulator: the six angle functions the two
+// need (q2, q3, q2+q3 for M(q); q1, q1+q2, q1+q2+q3 for the end effector) come from
+// three sincos and angle-addition products (the fp32 sums are rounded anyway);
+// everything else (and fp64, for bit-level parity) calls the two separately.
+template <int SYS, typename T>
+CACTO_D T stage_cost(const SysDev<T>& P, const CostDev<T>& C, const T* x, const T* u);
+template <int SYS, typename T>
+CACTO_D T cost_and_step(const SysDev<T>& P, const CostDev<T>& C, bool has_cost, const T* x, const T* u, T* xn) {
+  if constexpr (SYS == CACTO_SYS_MANIPULATOR3 && sizeof(T) == 4) {
+    T s1, c1, s2, c2, s3, c3;
+    m_sincos(x[0], &s1, &c1);
+    m_sincos(x[1], &s2, &c2);
+    m_sincos(x[2], &s3, &c3);
+    const T s23 = s2 * c3 + c2 * s3, c23 = c2 * c3 - s2 * s3;
+    T sc = T(0);
+    if (has_cost) {
+      const T s12 = s1 * c2 + c1 * s2, c12 = c1 * c2 - s1 * s2;
+      const T s123 = s1 * c23 + c1 * s23, c123 = c1 * c23 - s1 * s23;
+      const T px = P.len[0] * c1 + P.len[1] * c12 + P.len[2] * c123;
+      const T py = P.len[0] * s1 + P.len[1] * s12 + P.len[2] * s123;
+      T uu = u[0] * u[0];
+      uu += u[1] * u[1];
+      uu += u[2] * u[2];
+      sc = point_value(C, px, py) + C.w_u * uu;
+    }
+    T M[6], h[3], Mi[6], r[3], qdd[3];
+    manip_mass_trig(P, x + 3, s2, c2, s3, c3, s23, c23, M, h);
+    sym3_inverse(M, Mi);
+    r[0] = u[0] - h[0];
+    r[1] = u[1] - h[1];
+    r[2] = u[2] - h[2];
+    sym3_apply(Mi, r, qdd);
+    const T dt = P.dt;
+    xn[0] = x[0] + dt * x[3];
+    xn[1] = x[1] + dt * x[4];
+    xn[2] = x[2] + dt * x[5];
+    xn[3] = x[3] + dt * qdd[0];
+    xn[4] = x[4] + dt * qdd[1];
+    xn[5] = x[5] + dt * qdd[2];
+    return sc;
+  } else {
+    const T sc = has_cost ? stage_cost<SYS>(P, C, x, u) : T(0);
+    step<SYS>(P, x, u, xn);
+    return sc;
   }
 }
 

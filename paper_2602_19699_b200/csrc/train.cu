@@ -557,8 +557,7 @@ __global__ void __launch_bounds__(kThreads) actor_prep_kernel(const PrepArgs<T> 
       for (int c = 0; c < nn; ++c) x[c] = xa[c];
 #pragma unroll
       for (int j = 0; j < mm; ++j) u[j] = head_value(a.head, a.nc, j, OUT[j * S + s]);
-      a.lstage[base + s] = stage_cost<SYS>(a.sys, a.cost, x, u);
-      step<SYS>(a.sys, x, u, xn);
+      a.lstage[base + s] = cost_and_step<SYS>(a.sys, a.cost, true, x, u, xn);
       T* o = a.xn + (base + s) * (nn + 1);
 #pragma unroll
       for (int c = 0; c < nn; ++c) o[c] = xn[c];

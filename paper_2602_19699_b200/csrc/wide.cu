@@ -355,8 +355,7 @@ __global__ void actor_prep_rows_kernel(int64_t B, RowSrc xa, const float* __rest
     for (int c = 0; c < nn; ++c) x[c] = x0[c];
 #pragma unroll
     for (int j = 0; j < mm; ++j) u[j] = head_value(head, nc, j, O[b * ldo + j] + bL[j]);
-    LS[b] = stage_cost<SYS>(sys, cost, x, u);
-    step<SYS>(sys, x, u, xn);
+    LS[b] = cost_and_step<SYS>(sys, cost, true, x, u, xn);
 #pragma unroll
     for (int c = 0; c < nn; ++c) XN[b * (nn + 1) + c] = xn[c];
     XN[b * (nn + 1) + nn] = x0[nn] + 1.f;
