@@ -581,10 +581,11 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     // ---- MMA issuer --------------------------------------------------------------------
     const uint32_t i64 = tc::idesc_f16(HP), i16 = tc::idesc_f16(rtc::NOUT);
     auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
+    auto desc0 = [&](uint32_t off) { return tc::make_desc(sbase + off, rtc::W0_LBO, rtc::W0_SBO, 0); };
     const uint32_t ahi = tmem + TA_HI, alo = tmem + TA_LO;
     uint32_t pf = 0, pft = 0;
     auto fwd = [&](uint32_t so, int l, uint32_t dcol, uint32_t ah, uint32_t al) {
-      if (l == 0) issue<1>(dcol, ah, al, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), i64, false);
+      if (l == 0) issue<1>(dcol, ah, al, desc0(so + PL::off_w0), desc0(so + PL::off_w0 + PL::W0), i64, false);
       else if (l < 3)
         issue<4>(dcol, ah, al, desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH),
                  desc(so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH + PL::WH), i64, false);
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         } else if (k == 10) {
           issue<4>(tmem + TD, ahi, alo, desc(OFF_W0T), desc(OFF_W0T + W0T), i16, true);  // s_0
         } else if (k == 11) {
-          issue<1>(tmem + TD, ahi, alo, desc(PL::off_w0), desc(PL::off_w0 + PL::W0), i64, true);  // r_0
+          issue<1>(tmem + TD, ahi, alo, desc0(PL::off_w0), desc0(PL::off_w0 + PL::W0), i64, true);  // r_0
         } else if (k == 12 || k == 13) {
           const uint32_t wo = PL::off_wh + (uint32_t)(2 * (k - 12)) * PL::WH;
           issue<4>(tmem + TD, ahi, alo, desc(wo), desc(wo + PL::WH), i64, true);  // r_1, r_2

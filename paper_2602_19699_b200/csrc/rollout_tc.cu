@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     // ---- MMA issuer (whole warp converged; elect.sync picks the issuing lane) ----------
     const uint32_t idesc_h = tc::idesc_f16(HP), idesc_o = tc::idesc_f16(NOUT);
     auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
+    auto desc0 = [&](uint32_t off) { return tc::make_desc(sbase + off, W0_LBO, W0_SBO, 0); };
     uint32_t pf[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) pf[t] = 0;
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
           const uint32_t d = tmem + (uint32_t)(t * TM::PER_TILE), ahi = d + HP, alo = d + HP + HP / 2;
           const uint32_t bar = saddr(&done_bar[t]);
           if (l == 0) {
-            issue_layer_commit<KIN / 16>(d, ahi, alo, desc(so + PL::off_w0), desc(so + PL::off_w0 + PL::W0), idesc_h,
+            issue_layer_commit<KIN / 16>(d, ahi, alo, desc0(so + PL::off_w0), desc0(so + PL::off_w0 + PL::W0), idesc_h,
                                          bar);
           } else if (l < nh) {
             const uint32_t wo = so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;

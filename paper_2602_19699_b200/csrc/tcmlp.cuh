@@ -21,9 +21,18 @@ constexpr float LOG2E = 1.4426950408889634f;
 
 // shared-memory plan (bytes, from a 1024-aligned base); fp16 K-major SW128
 // operands: rows of 128 B = 64 halves
+// The input layer's weights (K = KIN = 16) use the no-swizzle K-major layout:
+// 8-row x 16-byte core matrices, the two K halves 128 B apart (LBO), 8-row groups
+// 256 B apart (SBO) -- 32 B per row instead of a 128-byte swizzle row with 96 B
+// unused (frees 12 KB of shared memory per network, i.e. L1 for K1's spills)
+CACTO_HD uint32_t w0_off(int r, int k) {
+  return (uint32_t)((r >> 3) * 256 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+constexpr uint32_t W0_LBO = 128, W0_SBO = 256;
+
 template <int HP>
 struct Plan {
-  static constexpr uint32_t W0 = HP * 128;    // [HP][16 used]
+  static constexpr uint32_t W0 = HP * 32;     // [HP][16], no-swizzle core matrices
   static constexpr uint32_t WH = HP * 128;    // [HP][HP]   (HP <= 64)
   static constexpr uint32_t WO = NOUT * 128;  // [16][HP]
   static constexpr uint32_t off_w0 = 0;       // hi, lo
@@ -106,6 +115,20 @@ CACTO_D void stage_w(unsigned char* hi, unsigned char* lo, const float* src, int
     const float v = (r < rows && c < cols) ? src[(int64_t)r * stride + c] * scale : 0.f;
     const __half h = __float2half_rn(v);
     const uint32_t o = sw128h(r, c);
+    *reinterpret_cast<__half*>(hi + o) = h;
+    *reinterpret_cast<__half*>(lo + o) = __float2half_rn(v - __half2float(h));
+  }
+}
+
+// the input layer's W (row-major [rows][cols], stride) * scale as hi/lo fp16 in the
+// no-swizzle K-major layout of w0_off (rrows x KIN, zero padded)
+CACTO_D void stage_w0(unsigned char* hi, unsigned char* lo, const float* src, int rows, int cols, int stride,
+                      float scale, int rrows, int tid, int nthr) {
+  for (int e = tid; e < rrows * KIN; e += nthr) {
+    const int r = e / KIN, c = e - r * KIN;
+    const float v = (r < rows && c < cols) ? src[(int64_t)r * stride + c] * scale : 0.f;
+    const __half h = __float2half_rn(v);
+    const uint32_t o = w0_off(r, c);
     *reinterpret_cast<__half*>(hi + o) = h;
     *reinterpret_cast<__half*>(lo + o) = __float2half_rn(v - __half2float(h));
   }
@@ -258,7 +281,7 @@ CACTO_D void stage_net(unsigned char* slot, const float* P, int nh, int in, int 
   using PL = rtc::Plan<HP>;
   const int64_t b0 = (int64_t)HP * IP;
   float* bias = reinterpret_cast<float*>(slot + PL::off_bias);
-  rtc::stage_w(slot + PL::off_w0, slot + PL::off_w0 + PL::W0, P, HP, in, IP, AF::S, HP, rtc::KIN, tid, nthr);
+  rtc::stage_w0(slot + PL::off_w0, slot + PL::off_w0 + PL::W0, P, HP, in, IP, AF::S, HP, tid, nthr);
   rtc::stage_bias(bias, P, P + b0, HP, in, IP, AF::S, false, HP, tid, nthr);
   int64_t off = b0 + HP;
   for (int i = 1; i < nh; ++i) {
