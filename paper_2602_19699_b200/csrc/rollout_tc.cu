@@ -68,6 +68,9 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   stage_net<HP, IP, AF>(base, a.params, nh, n + 1, m, threadIdx.x, NTHR);
   for (int p = 0; p < n_pre; ++p)
     stage_net<HP, IP, AF>(base + (p + 1) * PL::SLOT, a.pre_params[p], nh, n + 1, 1, threadIdx.x, NTHR);
+  // the bias MMAs' ones block, after the pairwise partial sums
+  const uint32_t off_ones = (uint32_t)(1 + n_pre) * PL::SLOT + (uint32_t)NTHR * 9 * 4;
+  if (CACTO_RTC_BIAS_MMA) stage_ones(base + off_ones, threadIdx.x, NTHR);
   if (threadIdx.x == 0) {
     for (int t = 0; t < NT; ++t) {
       tc::mbar_init(&full_bar[t], WPT);
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     uint32_t pd = 0;
     // D[my columns] <- scaled bias of layer l of the net in `slot` (l == nh: output)
     auto preload_bias = [&](int slot, int l) {
+      if (CACTO_RTC_BIAS_MMA) return;  // the MMA warp's first MMA of the layer writes it
       const uint32_t bias_s = sbase + (uint32_t)slot * PL::SLOT + PL::off_bias;
       if (l == nh) {
         if (part != 0) return;
@@ -290,6 +294,8 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     const uint32_t idesc_h = tc::idesc_f16(HP), idesc_o = tc::idesc_f16(NOUT);
     auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
     auto desc0 = [&](uint32_t off) { return tc::make_desc(sbase + off, W0_LBO, W0_SBO, 0); };
+    const uint64_t ones = tc::make_desc(sbase + off_ones, ONES_LBO, ONES_SBO, 0);
+    auto bdesc = [&](uint32_t off) { return tc::make_desc(sbase + off, BIAS_LBO, BIAS_SBO, 0); };
     uint32_t pf[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) pf[t] = 0;
@@ -305,13 +311,14 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
           const uint32_t bar = saddr(&done_bar[t]);
           if (l == 0) {
             issue_layer_commit<KIN / 16>(d, ahi, alo, desc0(so + PL::off_w0), desc0(so + PL::off_w0 + PL::W0), idesc_h,
-                                         bar);
+                                         bar, ones, bdesc(so + PL::off_bmma));
           } else if (l < nh) {
             const uint32_t wo = so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;
-            issue_layer_commit<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h, bar);
+            issue_layer_commit<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h, bar, ones,
+                                        bdesc(so + PL::off_bmma + (uint32_t)l * PL::BM_H));
           } else {
             issue_layer_commit<HP / 16>(d, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), idesc_o,
-                                        bar);
+                                        bar, ones, bdesc(so + PL::off_bmma_o));
           }
           __syncwarp();
         }
@@ -335,9 +342,10 @@ static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   auto kern = a.act == CACTO_ACT_ELU ? rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_ELU>
                                      : rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_TANH>;
   constexpr uint32_t ACC = (uint32_t)(NT * SPLIT * 128 + 32) * 9 * 4;  // pairwise partial sums
-  const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + ACC + 1024;
-  if (!ensure_smem((const void*)kern, 3 * PL::SLOT + ACC + 1024))
-    return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", 3 * PL::SLOT + ACC + 1024);
+  constexpr uint32_t ONES = CACTO_RTC_BIAS_MMA ? rtc::ONES_BYTES : 0;
+  const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + ACC + ONES + 1024;
+  if (!ensure_smem((const void*)kern, 3 * PL::SLOT + ACC + ONES + 1024))
+    return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", 3 * PL::SLOT + ACC + ONES + 1024);
   // starts per CTA: as even as 32-row granularity allows over whole waves of SMs
   // (65,536 starts: 147 CTAs of 448 instead of 128 CTAs of 512 leaving 20 SMs idle)
   const int64_t per = (int64_t)NT * rtc::TILE, sms = num_sms();

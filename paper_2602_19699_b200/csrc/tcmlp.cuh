@@ -39,8 +39,14 @@ struct Plan {
   static constexpr uint32_t off_wh = off_w0 + 2 * W0;  // (hi, lo) x (nh - 1), nh <= 3
   static constexpr uint32_t off_wo = off_wh + 2 * 2 * WH;
   static constexpr uint32_t off_bias = off_wo + 2 * WO;  // fp32 [3][HP] + [NOUT], scaled
+  // the same biases as B operands of one K = 16 MMA against a ones column block
+  // (bias_b_off: three fp16 parts h1 + h2 + h3 = the fp32 bias per row), so the
+  // MMA itself initialises D with the bias: [3][HP rows x 16 B] + [NOUT x 16 B] + pad
+  static constexpr uint32_t off_bmma = off_bias + (3 * HP + NOUT) * 4;
+  static constexpr uint32_t BM_H = HP * 16;
+  static constexpr uint32_t off_bmma_o = off_bmma + 3 * BM_H;
   // one network's slot (1024-aligned); slot 0 = actor, 1..2 = the scoring nets
-  static constexpr uint32_t SLOT = (off_bias + (3 * HP + NOUT) * 4 + 1023) / 1024 * 1024;
+  static constexpr uint32_t SLOT = (off_bmma_o + NOUT * 16 + 16 + 1023) / 1024 * 1024;
 };
 template <int HP, int NT>
 struct Tmem {
@@ -134,9 +140,29 @@ CACTO_D void stage_w0(unsigned char* hi, unsigned char* lo, const float* src, in
   }
 }
 
-// scaled bias of one layer: scale * (b - shift * rowsum(W)) over the real columns
+// bias MMA operands (no-swizzle K-major, 8-row core matrices 128 B apart = SBO):
+// row r of a bias block holds (h1, h2, h3, 0 x 5), the fp32 bias as three fp16
+// parts; the A block is 128 rows of (1, 1, 1, 0 x 13), so one K = 16 MMA with
+// enable_input_d = 0 writes D = h1 + h2 + h3 = the bias.  The bias block's second
+// K core (k = 8..15, LBO = 16 B) overlaps finite data and meets A's zeros.
+constexpr uint32_t BIAS_LBO = 16, BIAS_SBO = 128, ONES_LBO = 128, ONES_SBO = 256, ONES_BYTES = 128 * 32;
+CACTO_D uint32_t bias_b_off(int r) { return (uint32_t)((r >> 3) * 128 + (r & 7) * 16); }
+CACTO_D __half sat_h(float v) {
+  unsigned short h;
+  asm("cvt.rn.satfinite.f16.f32 %0, %1;" : "=h"(h) : "f"(v));
+  return __ushort_as_half(h);
+}
+CACTO_D void stage_ones(unsigned char* dst, int tid, int nthr) {
+  for (int e = tid; e < 128 * 16; e += nthr) {
+    const int r = e >> 4, k = e & 15;
+    *reinterpret_cast<__half*>(dst + w0_off(r, k)) = __float2half_rn(k < 3 ? 1.f : 0.f);
+  }
+}
+
+// scaled bias of one layer: scale * (b - shift * rowsum(W)) over the real columns;
+// bm != nullptr: also its bias-MMA block
 CACTO_D void stage_bias(float* dst, const float* W, const float* b, int rows, int cols, int stride, float scale,
-                        bool shift, int rrows, int tid, int nthr) {
+                        bool shift, int rrows, int tid, int nthr, unsigned char* bm = nullptr) {
   for (int r = tid; r < rrows; r += nthr) {
     float v = 0.f;
     if (r < rows) {
@@ -146,6 +172,16 @@ CACTO_D void stage_bias(float* dst, const float* W, const float* b, int rows, in
       v = scale * (b[r] - s);
     }
     dst[r] = v;
+    if (bm) {
+      const __half h1 = sat_h(v);
+      const float r1 = v - __half2float(h1);
+      const __half h2 = sat_h(r1);
+      const __half h3 = sat_h(r1 - __half2float(h2));
+      __half* o = reinterpret_cast<__half*>(bm + bias_b_off(r));
+      o[0] = h1; o[1] = h2; o[2] = h3;
+#pragma unroll
+      for (int k = 3; k < 8; ++k) o[k] = __float2half_rn(0.f);
+    }
   }
 }
 
@@ -168,32 +204,44 @@ CACTO_D void issue_layer(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, u
 // warp shares its scheduler with four busy epilogue warps, so every instruction on
 // this path delays the tile (a per-MMA elect + descriptor moves cost ~700 cycles
 // per layer, measured with a clock64 timeline)
+#ifndef CACTO_RTC_BIAS_MMA
+#define CACTO_RTC_BIAS_MMA 1
+#endif
+#if CACTO_RTC_BIAS_MMA
+// D = ones x bias (enable_input_d = 0), then every layer MMA accumulates
+#define RTC_BIAS_MMA "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %8, %5, q;\n\t"
+#else
+// D was pre-loaded with the bias by the epilogue (tcgen05.st)
+#define RTC_BIAS_MMA ""
+#endif
 template <int KSTEPS>
 CACTO_D void issue_layer_commit(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
-                                uint32_t bar);
+                                uint32_t bar, uint64_t bias_a, uint64_t bias_b);
 template <>
 CACTO_D void issue_layer_commit<1>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
-                                   uint32_t bar) {
+                                   uint32_t bar, uint64_t bias_a, uint64_t bias_b) {
   asm volatile(
-      "{\n\t.reg .pred e, p;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
-      "setp.eq.u32 p, 1, 1;\n\t"
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "setp.eq.u32 p, 1, 1;\n\tsetp.eq.u32 q, 1, 0;\n\t"
       "elect.sync r|e, 0xffffffff;\n\t"
       "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      RTC_BIAS_MMA
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
-      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar)
+      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar), "l"(bias_a), "l"(bias_b)
       : "memory");
 }
 template <>
 CACTO_D void issue_layer_commit<2>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
-                                   uint32_t bar) {
+                                   uint32_t bar, uint64_t bias_a, uint64_t bias_b) {
   asm volatile(
-      "{\n\t.reg .pred e, p;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
-      "setp.eq.u32 p, 1, 1;\n\t"
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "setp.eq.u32 p, 1, 1;\n\tsetp.eq.u32 q, 1, 0;\n\t"
       "elect.sync r|e, 0xffffffff;\n\t"
       "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      RTC_BIAS_MMA
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
@@ -202,17 +250,18 @@ CACTO_D void issue_layer_commit<2>(uint32_t d, uint32_t ahi, uint32_t alo, uint6
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
-      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar)
+      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar), "l"(bias_a), "l"(bias_b)
       : "memory");
 }
 template <>
 CACTO_D void issue_layer_commit<4>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
-                                   uint32_t bar) {
+                                   uint32_t bar, uint64_t bias_a, uint64_t bias_b) {
   asm volatile(
-      "{\n\t.reg .pred e, p;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
-      "setp.eq.u32 p, 1, 1;\n\t"
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "setp.eq.u32 p, 1, 1;\n\tsetp.eq.u32 q, 1, 0;\n\t"
       "elect.sync r|e, 0xffffffff;\n\t"
       "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      RTC_BIAS_MMA
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
@@ -229,7 +278,7 @@ CACTO_D void issue_layer_commit<4>(uint32_t d, uint32_t ahi, uint32_t alo, uint6
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
-      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar)
+      ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar), "l"(bias_a), "l"(bias_b)
       : "memory");
 }
 
@@ -282,18 +331,21 @@ CACTO_D void stage_net(unsigned char* slot, const float* P, int nh, int in, int 
   const int64_t b0 = (int64_t)HP * IP;
   float* bias = reinterpret_cast<float*>(slot + PL::off_bias);
   rtc::stage_w0(slot + PL::off_w0, slot + PL::off_w0 + PL::W0, P, HP, in, IP, AF::S, HP, tid, nthr);
-  rtc::stage_bias(bias, P, P + b0, HP, in, IP, AF::S, false, HP, tid, nthr);
+  rtc::stage_bias(bias, P, P + b0, HP, in, IP, AF::S, false, HP, tid, nthr, slot + PL::off_bmma);
   int64_t off = b0 + HP;
   for (int i = 1; i < nh; ++i) {
     unsigned char* hi = slot + PL::off_wh + (uint32_t)(2 * (i - 1)) * PL::WH;
     rtc::stage_w(hi, hi + PL::WH, P + off, HP, HP, HP, AF::S, HP, HP, tid, nthr);
-    rtc::stage_bias(bias + i * HP, P + off, P + off + (int64_t)HP * HP, HP, HP, HP, AF::S, AF::SHIFT, HP, tid, nthr);
+    rtc::stage_bias(bias + i * HP, P + off, P + off + (int64_t)HP * HP, HP, HP, HP, AF::S, AF::SHIFT, HP, tid, nthr,
+                    slot + PL::off_bmma + (uint32_t)i * PL::BM_H);
     off += (int64_t)HP * HP + HP;
   }
   rtc::stage_w(slot + PL::off_wo, slot + PL::off_wo + PL::WO, P + off, out, HP, HP, rtc::WSCALE, rtc::NOUT, HP, tid,
                nthr);
   rtc::stage_bias(bias + 3 * HP, P + off, P + off + (int64_t)out * HP, out, HP, HP, rtc::WSCALE, AF::SHIFT, rtc::NOUT,
-                  tid, nthr);
+                  tid, nthr, slot + PL::off_bmma_o);
+  // the pad after the output block (read through its second K core)
+  if (tid < 4) reinterpret_cast<uint32_t*>(slot + PL::off_bmma_o + rtc::NOUT * 16)[tid] = 0u;
 }
 
 }  // namespace cacto
