@@ -36,10 +36,19 @@
 #include "tc.cuh"
 #include "tcmlp.cuh"
 
+#ifndef CACTO_RTC_SELF
+#define CACTO_RTC_SELF 1
+#endif
+
 namespace cacto {
 
+// threads of a CTA: NT tiles x 4 SPLIT epilogue warps (+ the MMA warp unless a
+// leader warp of each tile issues its own MMAs)
+template <int NT, int SPLIT>
+constexpr int rtc_threads() { return NT * SPLIT * 128 + (CACTO_RTC_SELF ? 0 : 32); }
+
 template <int SYS, int HP, int NT, int SPLIT, int ACT>
-__global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(const RolloutArgs<float> a) {
+__global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel(const RolloutArgs<float> a) {
   using namespace rtc;
   using PL = Plan<HP>;
   using TM = Tmem<HP, NT>;
@@ -49,8 +58,8 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   constexpr int IP = (n + 1) <= 8 ? 8 : ((n + 1) <= 16 ? 16 : 32);  // padded W0 row stride
   constexpr int WPT = 4 * SPLIT;    // epilogue warps per tile (SPLIT per TMEM lane quadrant)
   constexpr int COLS = HP / SPLIT;  // accumulator columns per epilogue warp
-  constexpr int NTHR = NT * WPT * 32 + 32;
-  constexpr int MMA_WARP = NT * WPT;
+  constexpr int NTHR = rtc_threads<NT, SPLIT>();
+  constexpr int MMA_WARP = NT * WPT;  // == the warp count when the tiles self-issue
   static_assert(n + 1 <= KIN && m <= 8 && HP <= 64, "tensor-core rollout: n + 1 <= 16, m <= 8, HP <= 64");
   static_assert(COLS == 16 || COLS == 32 || COLS == 64, "16, 32 or 64 columns per epilogue warp");
 
@@ -79,13 +88,38 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
     s_kmax = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MMA_WARP) tc::tmem_alloc(&tmem_base_sh, TM::COLS);
+  const int alloc_warp = CACTO_RTC_SELF ? 0 : MMA_WARP;
+  if (warp == alloc_warp) tc::tmem_alloc(&tmem_base_sh, TM::COLS);
   tc::fence_async_smem();  // staged weights -> async proxy
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t sbase = saddr(base);
+
+  // ---- MMA issue of layer l of pass P for tile t (whole warp, converged) -----------
+  const uint32_t idesc_h = tc::idesc_f16(HP), idesc_o = tc::idesc_f16(NOUT);
+  const uint32_t off_ones_c = off_ones;
+  auto issue = [&](int P, int l, int t) {
+    auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
+    auto desc0 = [&](uint32_t off) { return tc::make_desc(sbase + off, W0_LBO, W0_SBO, 0); };
+    auto bdesc = [&](uint32_t off) { return tc::make_desc(sbase + off, BIAS_LBO, BIAS_SBO, 0); };
+    const uint64_t ones = tc::make_desc(sbase + off_ones_c, ONES_LBO, ONES_SBO, 0);
+    const uint32_t so = (uint32_t)(P < n_pre ? P + 1 : 0) * PL::SLOT;
+    const uint32_t d = tmem + (uint32_t)(t * TM::PER_TILE), ahi = d + HP, alo = d + HP + HP / 2;
+    const uint32_t bar = saddr(&done_bar[t]);
+    if (l == 0) {
+      issue_layer_commit<KIN / 16>(d, ahi, alo, desc0(so + PL::off_w0), desc0(so + PL::off_w0 + PL::W0), idesc_h, bar,
+                                   ones, bdesc(so + PL::off_bmma));
+    } else if (l < nh) {
+      const uint32_t wo = so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;
+      issue_layer_commit<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h, bar, ones,
+                                  bdesc(so + PL::off_bmma + (uint32_t)l * PL::BM_H));
+    } else {
+      issue_layer_commit<HP / 16>(d, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), idesc_o, bar,
+                                  ones, bdesc(so + PL::off_bmma_o));
+    }
+  };
 
   // ---- roles: epilogue warp w < MMA_WARP serves tile g = w / WPT, TMEM lanes
   //      32(w%4)..+31 = starts r of the tile, accumulator columns [part*COLS, +COLS);
@@ -184,18 +218,34 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       tc::tmem_st8(t_ahi, hv);
       tc::tmem_st8(t_alo, lv);
     };
-    auto handoff = [&]() {
+    // the tile's leader warp (one per tile, on scheduler g % 4) polls its MMA
+    // barrier and, self-issuing, issues its MMAs
+    const bool leader = (warp % WPT) == (CACTO_RTC_SELF ? (g & 3) : 0);
+    auto handoff = [&](int P, int l) {
       tc::tmem_wait_st();
       tc::tc_fence_before();
+#if CACTO_RTC_SELF
+      // A of layer l is in TMEM once every warp of the tile has passed here: the
+      // leader waits for the others in named barrier 1 + NT + g and issues
+      if (leader) {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + NT + g), "r"(WPT * 32) : "memory");
+        tc::tc_fence_after();
+        issue(P, l, g);
+      } else {
+        asm volatile("bar.arrive %0, %1;" ::"r"(1 + NT + g), "r"(WPT * 32) : "memory");
+      }
+#else
+      (void)P; (void)l;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full_bar[g]);
+#endif
     };
     auto wait_done = [&]() {
 #ifndef CACTO_RTC_POLL_ALL
       // one warp of the tile polls the MMA barrier; the tile's other epilogue warps
       // block in a named barrier (no polling instructions on their schedulers):
       // manipulator3 K1 3.84 -> 3.78 ms (profiles/README.md)
-      if ((warp % WPT) == 0) tc::mbar_wait_sleep(&done_bar[g], pd);
+      if (leader) tc::mbar_wait_sleep(&done_bar[g], pd);
       asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(WPT * 32) : "memory");
 #elif defined(CACTO_RTC_PLAIN_WAIT)
       tc::mbar_wait(&done_bar[g], pd);
@@ -209,7 +259,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
       const int slot = P < n_pre ? P + 1 : 0;
       write_input(slot, P < n_pre ? t0 : t0 + (P - n_pre));
       preload_bias(slot, 0);
-      handoff();
+      handoff(P, 0);
     };
     if (npass > 0) start_pass(0);
     for (int P = 0; P < npass; ++P) {
@@ -244,7 +294,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
           }
         }
         preload_bias(slot, l + 1);
-        handoff();
+        handoff(P, l + 1);
       }
       // output layer
       wait_done();
@@ -289,13 +339,8 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
         a.scores[gi] = a.score_mode == CACTO_SCORE_STD ? sig : (a.score_mode == CACTO_SCORE_GAP ? gap : sig * gap);
       }
     }
-  } else {
+  } else if (!CACTO_RTC_SELF) {
     // ---- MMA issuer (whole warp converged; elect.sync picks the issuing lane) ----------
-    const uint32_t idesc_h = tc::idesc_f16(HP), idesc_o = tc::idesc_f16(NOUT);
-    auto desc = [&](uint32_t off) { return tc::make_desc(sbase + off, 16, 1024, 2); };
-    auto desc0 = [&](uint32_t off) { return tc::make_desc(sbase + off, W0_LBO, W0_SBO, 0); };
-    const uint64_t ones = tc::make_desc(sbase + off_ones, ONES_LBO, ONES_SBO, 0);
-    auto bdesc = [&](uint32_t off) { return tc::make_desc(sbase + off, BIAS_LBO, BIAS_SBO, 0); };
     uint32_t pf[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) pf[t] = 0;
@@ -307,19 +352,7 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
           tc::mbar_wait_sleep(&full_bar[t], pf[t]);
           pf[t] ^= 1;
           tc::tc_fence_after();
-          const uint32_t d = tmem + (uint32_t)(t * TM::PER_TILE), ahi = d + HP, alo = d + HP + HP / 2;
-          const uint32_t bar = saddr(&done_bar[t]);
-          if (l == 0) {
-            issue_layer_commit<KIN / 16>(d, ahi, alo, desc0(so + PL::off_w0), desc0(so + PL::off_w0 + PL::W0), idesc_h,
-                                         bar, ones, bdesc(so + PL::off_bmma));
-          } else if (l < nh) {
-            const uint32_t wo = so + PL::off_wh + (uint32_t)(2 * (l - 1)) * PL::WH;
-            issue_layer_commit<HP / 16>(d, ahi, alo, desc(wo), desc(wo + PL::WH), idesc_h, bar, ones,
-                                        bdesc(so + PL::off_bmma + (uint32_t)l * PL::BM_H));
-          } else {
-            issue_layer_commit<HP / 16>(d, ahi, alo, desc(so + PL::off_wo), desc(so + PL::off_wo + PL::WO), idesc_o,
-                                        bar, ones, bdesc(so + PL::off_bmma_o));
-          }
+          issue(P, l, t);
           __syncwarp();
         }
       }
@@ -327,21 +360,21 @@ __global__ void __launch_bounds__(NT * SPLIT * 128 + 32, 1) rollout_tc_kernel(co
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == MMA_WARP) tc::tmem_dealloc(tmem, TM::COLS);
+  if (warp == alloc_warp) tc::tmem_dealloc(tmem, TM::COLS);
 }
 
 template <int SYS, int HP, int NT>
 static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   using PL = rtc::Plan<HP>;
   // 4 tiles: one epilogue warp per lane quadrant; fewer tiles: the columns are
-  // split over more warps (shorter per-layer epilogue latency), 544 threads max
+  // split over more warps (shorter per-layer epilogue latency), 512 threads max
 #ifndef CACTO_RTC_SPLIT4
 #define CACTO_RTC_SPLIT4 1
 #endif
   constexpr int SPLIT = NT == 4 ? CACTO_RTC_SPLIT4 : (NT == 2 ? (HP >= 32 ? 2 : 1) : (HP >= 64 ? 4 : HP / 16));
   auto kern = a.act == CACTO_ACT_ELU ? rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_ELU>
                                      : rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_TANH>;
-  constexpr uint32_t ACC = (uint32_t)(NT * SPLIT * 128 + 32) * 9 * 4;  // pairwise partial sums
+  constexpr uint32_t ACC = (uint32_t)rtc_threads<NT, SPLIT>() * 9 * 4;  // pairwise partial sums
   constexpr uint32_t ONES = CACTO_RTC_BIAS_MMA ? rtc::ONES_BYTES : 0;
   const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + ACC + ONES + 1024;
   if (!ensure_smem((const void*)kern, 3 * PL::SLOT + ACC + ONES + 1024))
@@ -355,7 +388,7 @@ static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   RolloutArgs<float> b = a;
   b.cta_rows = (int)rows;
   const int64_t blocks = (a.N + rows - 1) / rows;
-  kern<<<(unsigned)blocks, NT * SPLIT * 128 + 32, bytes, st>>>(b);
+  kern<<<(unsigned)blocks, rtc_threads<NT, SPLIT>(), bytes, st>>>(b);
   return check_launch("rollout_tc_kernel");
 }
 
