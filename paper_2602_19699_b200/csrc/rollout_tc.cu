@@ -29,6 +29,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "net.cuh"
 #include "rollout.cuh"
@@ -38,6 +39,9 @@
 
 #ifndef CACTO_RTC_SELF
 #define CACTO_RTC_SELF 1
+#endif
+#ifndef CACTO_RTC_CORE_OUT
+#define CACTO_RTC_CORE_OUT 1
 #endif
 
 namespace cacto {
@@ -62,6 +66,12 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
   constexpr int MMA_WARP = NT * WPT;  // == the warp count when the tiles self-issue
   static_assert(n + 1 <= KIN && m <= 8 && HP <= 64, "tensor-core rollout: n + 1 <= 16, m <= 8, HP <= 64");
   static_assert(COLS == 16 || COLS == 32 || COLS == 64, "16, 32 or 64 columns per epilogue warp");
+  // output layer on the CUDA cores (m <= 2, one warp per lane quadrant): the last
+  // hidden epilogue accumulates o = W_out v + b from the fp32 activations it just
+  // computed -- no output-layer MMAs, no hand-off / completion round trip, no TMEM
+  // traffic for that layer (fp32 FMAs: more accurate than the 3xFP16 products)
+  constexpr int MO = (CACTO_RTC_CORE_OUT && SPLIT == 1 && m <= 2) ? m : 0;
+  constexpr uint32_t WF = (uint32_t)(MO * HP + 4) * 4;  // fp32 W_out [MO][HP] + b [MO] per net
 
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
@@ -80,6 +90,26 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
   // the bias MMAs' ones block, after the pairwise partial sums
   const uint32_t off_ones = (uint32_t)(1 + n_pre) * PL::SLOT + (uint32_t)NTHR * 9 * 4;
   if (CACTO_RTC_BIAS_MMA) stage_ones(base + off_ones, threadIdx.x, NTHR);
+  const uint32_t off_wf = off_ones + ONES_BYTES;
+  if constexpr (MO > 0) {
+    // fp32 output layers (unscaled; rows past a net's outputs are zero)
+    const int64_t wo_off = (int64_t)HP * IP + HP + (int64_t)(nh - 1) * (HP * HP + HP);
+    for (int p = 0; p <= n_pre; ++p) {
+      const float* P = p == 0 ? a.params : a.pre_params[p - 1];
+      const int outs = p == 0 ? m : 1;
+      float* dst = (float*)(base + off_wf + (uint32_t)p * WF);
+      for (int e = threadIdx.x; e < MO * HP + MO; e += NTHR) {
+        float v = 0.f;
+        if (e < MO * HP) {
+          const int j = e / HP;
+          if (j < outs) v = P[wo_off + e];
+        } else if (e - MO * HP < outs) {
+          v = P[wo_off + (int64_t)outs * HP + (e - MO * HP)];
+        }
+        dst[e] = v;
+      }
+    }
+  }
   if (threadIdx.x == 0) {
     for (int t = 0; t < NT; ++t) {
       tc::mbar_init(&full_bar[t], WPT);
@@ -264,8 +294,51 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
     if (npass > 0) start_pass(0);
     for (int P = 0; P < npass; ++P) {
       const int slot = P < n_pre ? P + 1 : 0;
+      float oc[MO > 0 ? MO : 1];  // output-layer values (CUDA-core path)
       for (int l = 0; l < nh; ++l) {  // hidden layers
         wait_done();
+        if (MO > 0 && l == nh - 1) {
+          const uint32_t wf = sbase + off_wf + (uint32_t)(P < n_pre ? P + 1 : 0) * WF;
+          uint64_t acc[MO > 0 ? MO : 1];
+#pragma unroll
+          for (int j = 0; j < MO; ++j) acc[j] = 0ull;
+          float za[16], zb[16];
+          tc::tmem_ld16(t_d, za);
+          tc::tmem_wait_ld_dep(za);
+#pragma unroll
+          for (int c0 = 0; c0 < COLS; c0 += 16) {
+            if (c0 + 16 < COLS) tc::tmem_ld16(t_d + (uint32_t)(c0 + 16), zb);
+#pragma unroll
+            for (int c = 0; c < 16; c += 4) {
+              uint64_t v01, v23;
+              if constexpr (ACT == CACTO_ACT_ELU) {
+                v01 = elu2(za[c], za[c + 1], AF::S);
+                v23 = elu2(za[c + 2], za[c + 3], AF::S);
+              } else {
+                v01 = f2pack(AF::apply(za[c]), AF::apply(za[c + 1]));
+                v23 = f2pack(AF::apply(za[c + 2]), AF::apply(za[c + 3]));
+              }
+#pragma unroll
+              for (int j = 0; j < MO; ++j) {
+                const V4<float> w = lds4(wf + (uint32_t)((j * HP + c0 + c) * 4), (float*)nullptr);
+                acc[j] = f2fma(v01, f2pack(w.v[0], w.v[1]), acc[j]);
+                acc[j] = f2fma(v23, f2pack(w.v[2], w.v[3]), acc[j]);
+              }
+            }
+            if (c0 + 16 < COLS) {
+              tc::tmem_wait_ld_dep(zb);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) za[c] = zb[c];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < MO; ++j) {
+            float e0, e1;
+            f2unpack(acc[j], e0, e1);
+            oc[j] = (e0 + e1) + lds1(wf + (uint32_t)((MO * HP + j) * 4), (float*)nullptr);
+          }
+          break;
+        }
         // 16-column chunks, software pipelined: the next chunk's tcgen05.ld is in
         // flight while this chunk's activations are computed and stored (a single
         // warp's ld + wait costs ~160 cycles, profiles/probe_tmem.cu)
@@ -297,9 +370,14 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
         handoff(P, l + 1);
       }
       // output layer
-      wait_done();
       float o[16];
-      if (part == 0) tc::tmem_ld16_wait(t_d, o);
+      if constexpr (MO > 0) {
+#pragma unroll
+        for (int j = 0; j < MO; ++j) o[j] = oc[j] * WSCALE;  // the MMA path's scaled D
+      } else {
+        wait_done();
+        if (part == 0) tc::tmem_ld16_wait(t_d, o);
+      }
       if (slot != 0) {
         // scoring net: sigma(x0) = sigma_min + softplus(o) or V(x0) = o
         const float ov = o[0] * (1.f / WSCALE);
@@ -375,7 +453,7 @@ static int launch_rollout_tc_nt(const RolloutArgs<float>& a, cudaStream_t st) {
   auto kern = a.act == CACTO_ACT_ELU ? rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_ELU>
                                      : rollout_tc_kernel<SYS, HP, NT, SPLIT, CACTO_ACT_TANH>;
   constexpr uint32_t ACC = (uint32_t)rtc_threads<NT, SPLIT>() * 9 * 4;  // pairwise partial sums
-  constexpr uint32_t ONES = CACTO_RTC_BIAS_MMA ? rtc::ONES_BYTES : 0;
+  constexpr uint32_t ONES = (CACTO_RTC_BIAS_MMA ? rtc::ONES_BYTES : 0) + 3 * (3 * HP + 4) * 4;  // + fp32 output layers
   const uint32_t bytes = (uint32_t)(1 + a.n_pre) * PL::SLOT + ACC + ONES + 1024;
   if (!ensure_smem((const void*)kern, 3 * PL::SLOT + ACC + ONES + 1024))
     return set_error(CACTO_ECUDA, "rollout_tc: %u B of shared memory not available", 3 * PL::SLOT + ACC + ONES + 1024);

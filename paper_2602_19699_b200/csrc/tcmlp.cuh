@@ -293,7 +293,8 @@ CACTO_D void issue_layer_commit<4>(uint32_t d, uint32_t ahi, uint32_t alo, uint6
 template <int ACT>
 struct ActTC;
 
-CACTO_D void elu_split2(float d0, float d1, float S, uint32_t& hi, uint32_t& lo) {
+// the ELU pair alone (packed fp32x2)
+CACTO_D uint64_t elu2(float d0, float d1, float S) {
   using namespace rtc;
   const uint64_t d = f2pack(d0, d1), ad = f2pack(fabsf(d0), fabsf(d1));  // |.| folds into FADD2
   const uint64_t mn2 = f2sub(d, ad);   // 2 min(D, 0)
@@ -304,9 +305,12 @@ CACTO_D void elu_split2(float d0, float d1, float S, uint32_t& hi, uint32_t& lo)
   f2unpack(m, m0, m1);
   const uint64_t e = f2add(f2pack(tc::ex2_ftz(m0), tc::ex2_ftz(m1)), f2pack(-1.f, -1.f));
   const float is = 0.5f * (1.f / S);  // exactly half of fl(1/S)
-  const uint64_t v = f2fma(pos2, f2pack(is, is), e);
+  return f2fma(pos2, f2pack(is, is), e);
+}
+CACTO_D void elu_split2(float d0, float d1, float S, uint32_t& hi, uint32_t& lo) {
+  using namespace rtc;
   float v0, v1;
-  f2unpack(v, v0, v1);
+  f2unpack(elu2(d0, d1, S), v0, v1);
   split2(v0, v1, hi, lo);
 }
 
