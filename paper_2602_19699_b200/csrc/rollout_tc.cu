@@ -40,6 +40,9 @@
 #ifndef CACTO_RTC_SELF
 #define CACTO_RTC_SELF 1
 #endif
+#ifndef CACTO_RTC_SKIP_IDLE
+#define CACTO_RTC_SKIP_IDLE 1
+#endif
 #ifndef CACTO_RTC_CORE_OUT
 #define CACTO_RTC_CORE_OUT 1
 #endif
@@ -191,7 +194,13 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
   // passes: the scoring nets' forwards on [x0, t0], then the kmax actor steps
   const int npass = n_pre + kmax;
 
-  if (epi) {
+  // warps whose 32 starts all lie past the CTA's range (the last tile of a
+  // 448-row CTA has 2 of 4) skip the rollout: the tile's barriers count only its
+  // active warps, so the idle ones free their issue slots (K1 is issue bound)
+  const int tile_rows = min(TILE, max(0, a.cta_rows - g * TILE));
+  const int act_q = (CACTO_RTC_SKIP_IDLE && CACTO_RTC_SELF) ? (tile_rows + 31) >> 5 : 4;  // active quadrants of tile g
+  const int bar_n = act_q * SPLIT * 32;                                // threads on the tile's barriers
+  if (epi && q < act_q) {
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * TM::PER_TILE);
     const uint32_t t_d = lane_base, t_ahi = lane_base + HP, t_alo = lane_base + HP + HP / 2;
     const int c_base = part * COLS;
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
     };
     // the tile's leader warp (one per tile, on scheduler g % 4) polls its MMA
     // barrier and, self-issuing, issues its MMAs
-    const bool leader = (warp % WPT) == (CACTO_RTC_SELF ? (g & 3) : 0);
+    const bool leader = (warp % WPT) == (CACTO_RTC_SELF ? ((g & 3) < act_q ? (g & 3) : 0) : 0);
     auto handoff = [&](int P, int l) {
       tc::tmem_wait_st();
       tc::tc_fence_before();
@@ -258,11 +267,11 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
       // A of layer l is in TMEM once every warp of the tile has passed here: the
       // leader waits for the others in named barrier 1 + NT + g and issues
       if (leader) {
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + NT + g), "r"(WPT * 32) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + NT + g), "r"(bar_n) : "memory");
         tc::tc_fence_after();
         issue(P, l, g);
       } else {
-        asm volatile("bar.arrive %0, %1;" ::"r"(1 + NT + g), "r"(WPT * 32) : "memory");
+        asm volatile("bar.arrive %0, %1;" ::"r"(1 + NT + g), "r"(bar_n) : "memory");
       }
 #else
       (void)P; (void)l;
@@ -276,7 +285,7 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
       // block in a named barrier (no polling instructions on their schedulers):
       // manipulator3 K1 3.84 -> 3.78 ms (profiles/README.md)
       if (leader) tc::mbar_wait_sleep(&done_bar[g], pd);
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(WPT * 32) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(bar_n) : "memory");
 #elif defined(CACTO_RTC_PLAIN_WAIT)
       tc::mbar_wait(&done_bar[g], pd);
 #else
