@@ -49,6 +49,21 @@
 
 namespace cacto {
 
+#if CACTO_RTC_TIMELINE
+// clock64 timeline of one CTA's tile leaders (profiles/k1_timeline.py): [tile][pass
+// 20..27][layer 0..3][event: epilogue end, tile joined, issue end, MMA seen done]
+__device__ unsigned long long g_rtc_tl[4][8][4][4];
+#define RTC_TL(P, L, E)                                                                        \
+  do {                                                                                         \
+    if (blockIdx.x == 10 && lane == 0 && (P) >= 20 && (P) < 28 && (L) < 4)                    \
+      g_rtc_tl[g][(P)-20][L][E] = clock64();                                                   \
+  } while (0)
+#else
+#define RTC_TL(P, L, E) \
+  do {                  \
+  } while (0)
+#endif
+
 // threads of a CTA: NT tiles x 4 SPLIT epilogue warps (+ the MMA warp unless a
 // leader warp of each tile issues its own MMAs)
 template <int NT, int SPLIT>
@@ -206,6 +221,8 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
     const int c_base = part * COLS;
     float sig = 0.f, val = 0.f;  // scoring nets' outputs
     uint32_t pd = 0;
+    int tl_l = 0, tl_p = 0;  // layer / pass of the last issue (timeline)
+    (void)tl_l; (void)tl_p;
     // D[my columns] <- scaled bias of layer l of the net in `slot` (l == nh: output)
     auto preload_bias = [&](int slot, int l) {
       if (CACTO_RTC_BIAS_MMA) return;  // the MMA warp's first MMA of the layer writes it
@@ -267,9 +284,13 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
       // A of layer l is in TMEM once every warp of the tile has passed here: the
       // leader waits for the others in named barrier 1 + NT + g and issues
       if (leader) {
+        RTC_TL(P, l, 0);
         asm volatile("bar.sync %0, %1;" ::"r"(1 + NT + g), "r"(bar_n) : "memory");
+        RTC_TL(P, l, 1);
         tc::tc_fence_after();
         issue(P, l, g);
+        RTC_TL(P, l, 2);
+        tl_l = l; tl_p = P;
       } else {
         asm volatile("bar.arrive %0, %1;" ::"r"(1 + NT + g), "r"(bar_n) : "memory");
       }
@@ -284,7 +305,10 @@ __global__ void __launch_bounds__(rtc_threads<NT, SPLIT>(), 1) rollout_tc_kernel
       // one warp of the tile polls the MMA barrier; the tile's other epilogue warps
       // block in a named barrier (no polling instructions on their schedulers):
       // manipulator3 K1 3.84 -> 3.78 ms (profiles/README.md)
-      if (leader) tc::mbar_wait_sleep(&done_bar[g], pd);
+      if (leader) {
+        tc::mbar_wait_sleep(&done_bar[g], pd);
+        RTC_TL(tl_p, tl_l, 3);
+      }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(bar_n) : "memory");
 #elif defined(CACTO_RTC_PLAIN_WAIT)
       tc::mbar_wait(&done_bar[g], pd);
@@ -498,6 +522,15 @@ int launch_rollout_tc(const RolloutArgs<float>& a, cudaStream_t st) {
   if (nt == 4) return launch_rollout_tc_nt<SYS, HP, 4>(a, st);
   if (nt == 2) return launch_rollout_tc_nt<SYS, HP, 2>(a, st);
   return launch_rollout_tc_nt<SYS, HP, 1>(a, st);
+}
+
+extern "C" int cacto_debug_rtc_timeline(unsigned long long* host) {
+#if CACTO_RTC_TIMELINE
+  return cudaMemcpyFromSymbol(host, g_rtc_tl, sizeof(g_rtc_tl)) == cudaSuccess ? 0 : 1;
+#else
+  (void)host;
+  return -1;
+#endif
 }
 
 bool rollout_tc_enabled() {

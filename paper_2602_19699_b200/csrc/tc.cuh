@@ -43,6 +43,19 @@ CACTO_D void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(1000000u)
       : "memory");
 }
+// true on one lane of the (converged) warp.  Branching on it and issuing
+// unpredicated tcgen05 instructions inside costs ~4 SASS instructions per MMA
+// (R2UR of its operands); predicating each MMA on elect.sync's predicate costs
+// ~10 (per-MMA VOTEU / UMOV / PLOP3 / NOP around the R2URs)
+CACTO_D bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 CACTO_D void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 CACTO_D void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 CACTO_D void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

@@ -199,17 +199,18 @@ CACTO_D void issue_layer(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, u
   }
 }
 
-// one layer of one tile + its commit in ONE asm statement: a single elect.sync,
-// the 3 * KSTEPS MMAs (k-step offsets added in PTX) and the commit -- the issuing
-// warp shares its scheduler with four busy epilogue warps, so every instruction on
-// this path delays the tile (a per-MMA elect + descriptor moves cost ~700 cycles
-// per layer, measured with a clock64 timeline)
+// one layer of one tile + its commit in ONE asm statement issued by one elected
+// lane (branch, unpredicated MMAs: ~4 SASS instructions per MMA), the 3 * KSTEPS
+// MMAs (k-step offsets added in PTX) and the commit -- the issuing warp shares its
+// scheduler with busy epilogue warps, so every instruction on this path delays the
+// tile: with elect-predicated MMAs a hidden layer's issue took ~800 cycles of a
+// ~11.5k-cycle manipulator step (profiles/k1_timeline.py)
 #ifndef CACTO_RTC_BIAS_MMA
 #define CACTO_RTC_BIAS_MMA 1
 #endif
 #if CACTO_RTC_BIAS_MMA
 // D = ones x bias (enable_input_d = 0), then every layer MMA accumulates
-#define RTC_BIAS_MMA "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %8, %5, q;\n\t"
+#define RTC_BIAS_MMA "tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %8, %5, q;\n\t"
 #else
 // D was pre-loaded with the bias by the epilogue (tcgen05.st)
 #define RTC_BIAS_MMA ""
@@ -220,66 +221,66 @@ CACTO_D void issue_layer_commit(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t
 template <>
 CACTO_D void issue_layer_commit<1>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
                                    uint32_t bar, uint64_t bias_a, uint64_t bias_b) {
-  asm volatile(
-      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+  if (tc::elect_one()) asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
       "setp.eq.u32 p, 1, 1;\n\tsetp.eq.u32 q, 1, 0;\n\t"
-      "elect.sync r|e, 0xffffffff;\n\t"
       "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
       RTC_BIAS_MMA
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
       ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar), "l"(bias_a), "l"(bias_b)
       : "memory");
+  __syncwarp();
 }
 template <>
 CACTO_D void issue_layer_commit<2>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
                                    uint32_t bar, uint64_t bias_a, uint64_t bias_b) {
-  asm volatile(
-      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+  if (tc::elect_one()) asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
       "setp.eq.u32 p, 1, 1;\n\tsetp.eq.u32 q, 1, 0;\n\t"
-      "elect.sync r|e, 0xffffffff;\n\t"
       "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
       RTC_BIAS_MMA
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
       "add.u32 ah, %1, 8;\n\tadd.u32 al, %2, 8;\n\tadd.u64 bh, %3, 2;\n\tadd.u64 bl, %4, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
       ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar), "l"(bias_a), "l"(bias_b)
       : "memory");
+  __syncwarp();
 }
 template <>
 CACTO_D void issue_layer_commit<4>(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc,
                                    uint32_t bar, uint64_t bias_a, uint64_t bias_b) {
-  asm volatile(
-      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 r, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+  if (tc::elect_one()) asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
       "setp.eq.u32 p, 1, 1;\n\tsetp.eq.u32 q, 1, 0;\n\t"
-      "elect.sync r|e, 0xffffffff;\n\t"
       "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
       RTC_BIAS_MMA
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
       "add.u32 ah, %1, 8;\n\tadd.u32 al, %2, 8;\n\tadd.u64 bh, %3, 2;\n\tadd.u64 bl, %4, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
       "add.u32 ah, %1, 16;\n\tadd.u32 al, %2, 16;\n\tadd.u64 bh, %3, 4;\n\tadd.u64 bl, %4, 4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
       "add.u32 ah, %1, 24;\n\tadd.u32 al, %2, 24;\n\tadd.u64 bh, %3, 6;\n\tadd.u64 bl, %4, 6;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
       ::"r"(d), "r"(ahi), "r"(alo), "l"(whi), "l"(wlo), "r"(idesc), "r"(bar), "l"(bias_a), "l"(bias_b)
       : "memory");
+  __syncwarp();
 }
 
 }  // namespace rtc
