@@ -99,15 +99,20 @@ CACTO_D void stage_wt(unsigned char* hi, unsigned char* lo, const float* W, int 
 
 // one product layer: KSTEPS k-steps of 3 MMAs; `zero` starts a fresh accumulator
 template <int KSTEPS>
+// (one elected lane in a branch issues unpredicated MMAs: fewer instructions per
+// MMA on the layer chain than elect-predicated ones, tcmlp.cuh issue_layer_commit)
 CACTO_D void issue(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t whi, uint64_t wlo, uint32_t idesc, bool zero) {
+  if (tc::elect_one()) {
 #pragma unroll
-  for (int kk = 0; kk < KSTEPS; ++kk) {
-    const uint64_t wo = (uint64_t)(kk * 2);
-    const uint32_t ao = (uint32_t)(kk * 8);
-    tc::mma_f16_ts_elect(d, ahi + ao, whi + wo, idesc, (zero && kk == 0) ? 0u : 1u);
-    tc::mma_f16_ts_elect(d, ahi + ao, wlo + wo, idesc, 1u);
-    tc::mma_f16_ts_elect(d, alo + ao, whi + wo, idesc, 1u);
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+      const uint64_t wo = (uint64_t)(kk * 2);
+      const uint32_t ao = (uint32_t)(kk * 8);
+      tc::mma_f16_ts(d, ahi + ao, whi + wo, idesc, (zero && kk == 0) ? 0u : 1u);
+      tc::mma_f16_ts(d, ahi + ao, wlo + wo, idesc, 1u);
+      tc::mma_f16_ts(d, alo + ao, whi + wo, idesc, 1u);
+    }
   }
+  __syncwarp();
 }
 
 // derivative factors of the activation at z (nets.py:27-52): d1 = act'(z),
