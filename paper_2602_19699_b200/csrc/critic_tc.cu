@@ -916,15 +916,17 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
       tc::mbar_wait(&full_bar[s], (kb / WG_STAGES) & 1);
       tc::tc_fence_after();
       const uint32_t st0 = sb + (uint32_t)s * WG_STAGE;
+      if (tc::elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < WG_KB / 16; ++kk) {
-        const uint64_t ad = tc::make_desc(st0 + kk * 32, 16, 1024, 2);
-        const uint64_t bhi = tc::make_desc(st0 + WG_A + kk * 32, 16, 1024, 2);
-        const uint64_t blo = tc::make_desc(st0 + WG_A + WG_B + kk * 32, 16, 1024, 2);
-        tc::mma_f16_ss_elect(tmem, ad, bhi, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-        tc::mma_f16_ss_elect(tmem, ad, blo, idesc, 1u);
+        for (int kk = 0; kk < WG_KB / 16; ++kk) {
+          const uint64_t ad = tc::make_desc(st0 + kk * 32, 16, 1024, 2);
+          const uint64_t bhi = tc::make_desc(st0 + WG_A + kk * 32, 16, 1024, 2);
+          const uint64_t blo = tc::make_desc(st0 + WG_A + WG_B + kk * 32, 16, 1024, 2);
+          tc::mma_f16_ss(tmem, ad, bhi, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_f16_ss(tmem, ad, blo, idesc, 1u);
+        }
+        tc::tc_commit(&empty_bar[s]);
       }
-      tc::tc_commit_elect(&empty_bar[s]);
       __syncwarp();
     }
     tc::tc_commit_elect(&acc_bar);

@@ -143,6 +143,16 @@ CACTO_D void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t 
       : "memory");
 }
 
+// both operands in shared memory, unpredicated (inside `if (elect_one())`)
+CACTO_D void mma_f16_ss(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // kind::f16 MMA with both operands in shared memory (K-major descriptors)
 CACTO_D void mma_f16_ss_elect(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
