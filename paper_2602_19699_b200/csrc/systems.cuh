@@ -31,6 +31,7 @@ struct CostDev {
   T ocx[CACTO_MAX_OBST], ocy[CACTO_MAX_OBST];
   T e00[CACTO_MAX_OBST], e01[CACTO_MAX_OBST], e10[CACTO_MAX_OBST], e11[CACTO_MAX_OBST];
   T w_o, w_r, rho2, w_u, w_d;
+  T inv_rho2;  // fp32 path: -q * (1 / rho2) instead of an IEEE division per step
   T w_vel, w_vbar, v_max2, obs_r2, w_wall;
 };
 
@@ -87,6 +88,7 @@ CostDev<T> cost_dev(const cacto_cost_t& c) {
   d.w_o = (T)c.w_obstacle;
   d.w_r = (T)c.w_reward;
   d.rho2 = (T)(c.reward_radius * c.reward_radius);
+  d.inv_rho2 = (T)(1.0 / (c.reward_radius * c.reward_radius));
   d.w_u = (T)c.w_control;
   d.w_d = (T)c.w_distance;
   d.w_vel = (T)c.extra[0];
@@ -155,7 +157,9 @@ CACTO_D void sym3_inverse(const T M[6], T Mi[6]) {
   T c01 = M[2] * M[4] - M[1] * M[5];
   T c02 = M[1] * M[4] - M[2] * M[3];
   T det = M[0] * c00 + M[1] * c01 + M[2] * c02;
-  T id = T(1) / det;
+  T id;
+  if constexpr (sizeof(T) == 4) id = __frcp_rn(det);  // == 1.f / det (IEEE rn), no division slow path
+  else id = T(1) / det;
   Mi[0] = c00 * id;
   Mi[1] = c01 * id;
   Mi[2] = c02 * id;
@@ -293,8 +297,15 @@ CACTO_D T point_value(const CostDev<T>& C, T px, T py) {
   T rx = px - C.tx, ry = py - C.ty;
   T q = rx * rx + ry * ry;
   T val = C.w_d * q;
-  val -= C.w_r * cost_exp(-q / C.rho2);
-  for (int i = 0; i < C.n_obs; ++i) {
+  // fp64 keeps NumPy's division (bit-level parity); fp32 multiplies by the
+  // reciprocal (<= 1.5 ulp, as the input normalisation does)
+  if constexpr (sizeof(T) == 4) val -= C.w_r * cost_exp(-q * C.inv_rho2);
+  else val -= C.w_r * cost_exp(-q / C.rho2);
+  // unrolled over the (uniform) obstacle count: no loop-carried index / constant-bank
+  // address arithmetic per obstacle
+#pragma unroll
+  for (int i = 0; i < CACTO_MAX_OBST; ++i) {
+    if (i >= C.n_obs) break;
     T dx = px - C.ocx[i], dy = py - C.ocy[i];
     T e = dx * (C.e00[i] * dx + C.e01[i] * dy) + dy * (C.e10[i] * dx + C.e11[i] * dy);
     val += C.w_o * cost_softplus(T(10) * (T(1) - e));
