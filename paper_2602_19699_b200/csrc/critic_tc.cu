@@ -33,6 +33,22 @@ int gemm_tf32_partials(int M, int N, int K, const float* A, int64_t sam, int64_t
                        int64_t sbk, float alpha, int passes, void* ws, size_t ws_bytes, int* splits_out,
                        cudaStream_t st);
 
+#if CACTO_CTC_TIMELINE
+// clock64 timeline of CTA 10's second tile (profiles/critic_timeline.py):
+// [critic-chain layer 0..11][0: MMA warp saw the hand-off, 1: MMAs + commit issued,
+// 2: epilogue warp 0 saw the completion, 3: epilogue warp 0 handed the next layer off]
+__device__ unsigned long long g_ctc_tl[12][4];
+#define CTC_TL(I, E, T)                                                                 \
+  do {                                                                                  \
+    if (blockIdx.x == 10 && (T) == blockIdx.x + gridDim.x && lane == 0 && (I) < 12)     \
+      g_ctc_tl[I][E] = clock64();                                                       \
+  } while (0)
+#else
+#define CTC_TL(I, E, T) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace ctc {
 
 constexpr int HP = 64;
@@ -247,11 +263,17 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     const uint32_t bias_c = sbase + PL::off_bias, bias_t = sbase + SLOT + PL::off_bias;
     uint32_t pd = 0, pdt = 0;
     float loss_acc = 0.f;
+    int tl_w = 0, tl_h = 0;  // timeline counters (warp 0)
+    int64_t tl_t = 0;
+    (void)tl_w; (void)tl_h; (void)tl_t;
     auto handoff = [&]() {
       tc::tmem_wait_st();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full_bar);
+#if CACTO_CTC_TIMELINE
+      if (warp == 0) { CTC_TL(tl_h, 3, tl_t); ++tl_h; }
+#endif
     };
     auto handoff_t = [&]() {
       tc::tmem_wait_st();
@@ -266,6 +288,9 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     };
     auto wait_done = [&]() {
       tc::mbar_wait(&done_bar, pd);
+#if CACTO_CTC_TIMELINE
+      if (warp == 0) { CTC_TL(tl_w, 2, tl_t); ++tl_w; }
+#endif
       pd ^= 1;
       tc::tc_fence_after();
     };
@@ -332,6 +357,8 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     };
 
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      tl_w = tl_h = 0;
+      tl_t = t;
       const int64_t gb = t * TILE + r;
       const bool valid = gb < B;
       const int64_t rr = valid ? a.b.row(gb) : 0;
@@ -416,14 +443,15 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
 #pragma unroll
         for (int c = 0; c < 16; ++c) av[c] = AF::apply(z[c]);
         put_a(av);
+        if (l < 2) preload_bias(TZ + 64 * (l + 1), bias_c, l + 1);
+        else preload_out_bias(bias_c);
+        handoff();
+        // factor stores after the hand-off: the next layer's MMAs do not wait for them
         if (valid) {
           float* row = a.UA[l + 1] + (B + gb) * 68;
           st16g(row + c0, av);
           if (owner) *reinterpret_cast<float4*>(row + 64) = make_float4(1.f, 0.f, 0.f, 0.f);
         }
-        if (l < 2) preload_bias(TZ + 64 * (l + 1), bias_c, l + 1);
-        else preload_out_bias(bias_c);
-        handoff();
       }
       if (boot) {
         wait_done_t();
@@ -456,9 +484,9 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           g[c] = d1 * w3[c0 + c];
         }
         st16(TG + 128 + c0, g);
-        if (valid) st16g(a.GZ[2] + gb * 64 + c0, g);
         put_ab(g);
         handoff();  // S2: s_2 = g_2 W_2
+        if (valid) st16g(a.GZ[2] + gb * 64 + c0, g);
       }
       for (int l = 1; l >= 0; --l) {  // g_l = act'(z_l) s_{l+1}
         wait_done();
@@ -471,9 +499,9 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           g[c] = d1 * s[c] * RS;
         }
         st16(TG + 64 * l + c0, g);
-        if (valid) st16g(a.GZ[l] + gb * 64 + c0, g);
         put_ab(g);
         handoff();  // S1: s_1 = g_1 W_1 ; S0: s_0 = g_0 W_0 (N = 16)
+        if (valid) st16g(a.GZ[l] + gb * 64 + c0, g);
       }
       // errors, loss, u_0 (nets.py:268-277)
       wait_done();
@@ -518,13 +546,13 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         }
         st16(TG + 64 * l + c0, g);
         if (l < 2) {
+          put_ab(u);
+          handoff();  // R1, R2
           if (valid) {
             float* row = a.UA[l + 1] + gb * 68;
             st16g(row + c0, u);
             if (owner) *reinterpret_cast<float4*>(row + 64) = make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          put_ab(u);
-          handoff();  // R1, R2
         } else {
           if (valid) {
             float* row = a.UA[3] + gb * 68;
@@ -552,9 +580,9 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         }
         asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory");  // del_sh reused next tile
       }
-      if (valid) st16g(a.GZ[2] + (B + gb) * 64 + c0, zb);
       put_ab(zb);
       handoff();  // B2: abar_2 = zbar_2 W_2
+      if (valid) st16g(a.GZ[2] + (B + gb) * 64 + c0, zb);
       for (int l = 1; l >= 0; --l) {
         wait_done();
         float ab[16], z[16], zeta[16];
@@ -565,11 +593,11 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           d1h<ACT>(z[c] * (1.f / S), d1, h);
           zb[c] = d1 * ab[c] * RS + zeta[c];
         }
-        if (valid) st16g(a.GZ[l] + (B + gb) * 64 + c0, zb);
         if (l == 1) {
           put_ab(zb);
           handoff();  // B1: abar_1 = zbar_1 W_1
         }
+        if (valid) st16g(a.GZ[l] + (B + gb) * 64 + c0, zb);
       }
     }
     // loss partial of this CTA
@@ -607,14 +635,17 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           __syncwarp();
         }
         tc::mbar_wait(&full_bar, pf);
+        CTC_TL(l, 0, t);
         pf ^= 1;
         tc::tc_fence_after();
         fwd(0, l, l < 3 ? tmem + TZ + 64 * l : tmem + TD, ahi, alo);
         tc::tc_commit_elect(&done_bar);
         __syncwarp();
+        CTC_TL(l, 1, t);
       }
       for (int k = 8; k < 16; ++k) {  // sweep, gradient path, value path
         tc::mbar_wait(&full_bar, pf);
+        CTC_TL(k - 4, 0, t);
         pf ^= 1;
         tc::tc_fence_after();
         if (k == 8) {
@@ -635,6 +666,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         }
         tc::tc_commit_elect(&done_bar);
         __syncwarp();
+        CTC_TL(k - 4, 1, t);
       }
     }
   }
@@ -1088,6 +1120,15 @@ static AuxStream* aux_stream(cudaStream_t st) {
     }
   }
   return &x;
+}
+
+extern "C" int cacto_debug_ctc_timeline(unsigned long long* host) {
+#if CACTO_CTC_TIMELINE
+  return cudaMemcpyFromSymbol(host, g_ctc_tl, sizeof(g_ctc_tl)) == cudaSuccess ? 0 : 1;
+#else
+  (void)host;
+  return -1;
+#endif
 }
 
 int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_batch_t* bt, double k_s, void* ws,

@@ -80,6 +80,8 @@ def main():
     ap.add_argument("--batch", default="4096,65536,262144,1048576")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--no-torch", action="store_true")
+    ap.add_argument("--timeline", action="store_true",
+                    help="print the per-layer clock64 timeline of the last update (CACTO_CTC_TIMELINE=1 build)")
     args = ap.parse_args()
     set_precision("fp32")
     dev = torch.device("cuda:0")
@@ -150,6 +152,18 @@ def main():
                 del Ws, bs, tg, opt, xa_d, xk_d, vb, vbx
                 torch.cuda.empty_cache()
             print(json.dumps(line), flush=True)
+    if args.timeline:
+        buf = (ctypes.c_ulonglong * 48)()
+        assert _lib.load().cacto_debug_ctc_timeline(buf) == 0
+        t = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(12, 4)
+        t = t - t[0, 0]
+        # per critic-chain layer: hand-off seen by the MMA warp, MMAs issued, completion
+        # seen by epilogue warp 0, next hand-off by warp 0
+        rows = [dict(layer=i, mma_seen=int(t[i, 0]), issued=int(t[i, 1] - t[i, 0]),
+                     done_after_issue=int(t[i, 2] - t[i, 1]),
+                     epilogue=int(t[i + 1, 3] - t[i, 2]) if i + 1 < 12 else None,
+                     handoff_to_mma=int(t[i + 1, 0] - t[i + 1, 3]) if i + 1 < 12 else None) for i in range(12)]
+        print(json.dumps({"critic_tc_timeline_cycles": rows, "tile_cycles": int(t[11, 2] - t[0, 0])}), flush=True)
 
 
 if __name__ == "__main__":
