@@ -578,7 +578,9 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           d1h<ACT>(z[c] * (1.f / S), d1, h);
           zb[c] = d1 * (dlt * w3[c0 + c]) + zeta[c];
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory");  // del_sh reused next tile
+        // no second barrier before the next tile rewrites del_sh: that happens >= 10
+        // layer hand-offs later, each needing all 16 epilogue warps (full_bar), so
+        // every read above is done by then
       }
       put_ab(zb);
       handoff();  // B2: abar_2 = zbar_2 W_2
