@@ -52,10 +52,10 @@ WORKLOADS = {"dubins": 65536, "pointmass": 750, "manipulator3": 262144, "aliengo
 HIDDEN = 64
 CAND_MULT = 10
 SEED = 0
-# e2e: warm starts written zero-copy into pinned host memory by the take kernel (1) or
-# taken on the device and copied by the copy engine (0, measured faster: the 31.5 MB
-# of manipulator3 warm starts stream at full PCIe rate from a copy, not from SM stores)
-E2E_ZC_U = os.environ.get("CACTO_E2E_ZC_U", "0") == "1"
+# e2e: the warm starts go to a pinned host buffer through the public call's u_out; the
+# library takes them in chunks and copies each chunk with the copy engine while the next
+# chunk's take runs (CACTO_WARM_ZEROCOPY=1: the take kernel writes the host buffer
+# directly, measured slower -- SM stores over PCIe stream below the copy engine's rate)
 
 
 # ---------------------------------------------------------------------------------
@@ -514,14 +514,13 @@ def main():
         # the public call with HOST buffers: the rollout kernel reads the pinned x0
         # zero-copy and the take kernel writes the warm starts into pinned U_host
         # (both transfers cross PCIe inside the step, overlapped with the kernels)
-        uo = U_host if E2E_ZC_U else None
         if world == 1:
-            out = pipe.run(x0_pinned, keep_global, u_out=uo)
+            out = pipe.run(x0_pinned, keep_global, u_out=U_host)
         else:
-            out = pipe.run_sharded(x0_pinned, keep_global, base, dsel=dsel, u_out=uo)
+            out = pipe.run_sharded(x0_pinned, keep_global, base, dsel=dsel, u_out=U_host)
         order_host.copy_(out["order"], non_blocking=True)
         k = out["U"].shape[0]
-        if uo is None:
+        if out["U"].is_cuda:
             U_host[:k].copy_(out["U"], non_blocking=True)
         d2h_rows[0] = k
 

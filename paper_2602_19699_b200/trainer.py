@@ -29,6 +29,11 @@ import os
 # step 4.12 -> 4.19 ms, dubins 0.83 -> 0.90 ms, profiles/README.md).
 # CACTO_WARM_TMAJOR=0 selects start-major (A/B only).
 _TMAJOR = os.environ.get("CACTO_WARM_TMAJOR", "1") == "1"
+# host warm-start output: the take kernel writes the pinned host buffer directly
+# (zero-copy, "1") or runs in chunks whose device-to-host copies on a side stream
+# overlap the next chunk's take ("0", default; measured faster)
+_WARM_ZC = os.environ.get("CACTO_WARM_ZEROCOPY", "0") == "1"
+_WARM_CHUNKS = int(os.environ.get("CACTO_WARM_CHUNKS", "4"))
 
 
 def _dev(x0: torch.Tensor) -> torch.device:
@@ -143,6 +148,7 @@ class BicPipeline:
         self.costd = specs.cost_struct(model, field)
         self.base_index = base_index
         self.ws = SelectWorkspace()
+        self._copy_stream = None  # side stream of the chunked warm-start copies
         self.kernel_launches = 0
 
     def _u_all(self, N, T, dt, dev):
@@ -217,13 +223,43 @@ class BicPipeline:
         T = self.model.t_max - t0
         dt = torch_dtype(self.precision)
         if out is not None and reuse:
-            U = out[:K]
-            if U.dtype != dt or tuple(U.shape[1:]) != (T, self.model.m) or not U.is_contiguous():
+            if out[:K].dtype != dt or tuple(out.shape[1:]) != (T, self.model.m) or not out.is_contiguous():
                 raise ValueError("warm-start output buffer does not match [K, T, m] / dtype")
+        if out is not None and reuse and _WARM_ZC:
+            U = out[:K]
         else:
             U = torch.empty((K, T, self.model.m), device=_dev(x0), dtype=dt)
         if K == 0:
-            return U, 0
+            return (out[:0] if out is not None else U), 0
+        if reuse and out is not None and not _WARM_ZC and _TMAJOR and not out.is_cuda:
+            # chunked take; chunk c's copy to the pinned host buffer (side stream, copy
+            # engine) overlaps chunk c + 1's take; the caller's stream waits for the
+            # last copy, so the returned host rows are complete in stream order
+            main = torch.cuda.current_stream()
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(device=_dev(x0))
+            cs = self._copy_stream
+            row = T * self.model.m
+            es = U.element_size()
+            nch = max(1, min(_WARM_CHUNKS, K))
+            bounds = [K * c // nch for c in range(nch + 1)]
+            for c in range(nch):
+                c0, c1 = bounds[c], bounds[c + 1]
+                if c1 == c0:
+                    continue
+                _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), row, N,
+                          sel.data_ptr() + c0 * sel.element_size(), c1 - c0, U.data_ptr() + c0 * row * es,
+                          main.cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                cs.wait_event(ev)
+                with torch.cuda.stream(cs):
+                    out[c0:c1].copy_(U[c0:c1], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cs)
+            main.wait_event(done)
+            U.record_stream(cs)
+            return out[:K], nch
         if reuse:
             # the kept starts' controls from the cost rollout (same actor, start and t0:
             # the trajectories trainer.py:192-193 would roll out again)
@@ -233,6 +269,9 @@ class BicPipeline:
             else:
                 _lib.call("cacto_take_rows", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
                           sel.data_ptr(), K, U.data_ptr(), _stream())
+            if out is not None and U.is_cuda and not out.is_cuda:
+                out[:K].copy_(U, non_blocking=True)
+                U = out[:K]
             return U, 1
         kept = x0.to(_dev(x0)).index_select(0, sel)
         _lib.call("cacto_rollout", self.sysd, None, self.actor.desc, kept.data_ptr(), None, t0, K, T,

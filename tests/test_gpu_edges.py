@@ -316,11 +316,14 @@ np.savez(sys.argv[1], loss=loss, *g)
             assert np.abs(o[f"arr_{i}"] - r).max() <= 1e-4 * scale, i
 
 
-def test_bic_pipeline_host_buffers_zero_copy():
+@pytest.mark.parametrize("zero_copy", [False, True])
+def test_bic_pipeline_host_buffers_zero_copy(zero_copy, monkeypatch):
     """BicPipeline.run with a pinned HOST x0 (read zero-copy by the rollout kernel) and
-    a pinned host warm-start buffer (written by the take kernel) gives exactly the
+    a pinned host warm-start buffer (chunked take + copy-engine copies overlapped on a
+    side stream, or written zero-copy by the take kernel) gives exactly the
     device-resident results."""
     from bench import make_nets, candidates
+    monkeypatch.setattr(B_trainer, "_WARM_ZC", zero_copy)
     old = P.get_precision()
     P.set_precision("fp32")
     try:
