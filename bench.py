@@ -462,14 +462,14 @@ def main():
         dsel = parallel.DistributedSelect(N, keep_global, torch.float32 if args.precision == "fp32" else torch.float64)
     flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")  # > 126 MB L2
 
-    def step(x0):
+    def step(x0, u_out=None):
         if world == 1:
-            out = pipe.run(x0, keep_global)
+            out = pipe.run(x0, keep_global, u_out=u_out)
             return out["order"], out["U"]
         # shard-local K1+K2, the distributed exact select, and this rank's own
         # winners' warm starts (taken from its cost rollout): no states or controls
         # cross ranks, only the threshold histograms, counts and the keep winners
-        out = pipe.run_sharded(x0, keep_global, base, dsel=dsel)
+        out = pipe.run_sharded(x0, keep_global, base, dsel=dsel, u_out=u_out)
         return out["order"], out["U"]
 
     def timed(fn, K, W):
@@ -537,10 +537,10 @@ def main():
 
     def e2e_seeded_step():
         sample_initial_states_device(spec, N * world, SEED, first_row=base, rows=N, out=x0_seeded)
-        order, U = step(x0_seeded)
+        order, U = step(x0_seeded, u_out=U_host)
         order_host.copy_(order, non_blocking=True)
-        k = U.shape[0]
-        U_host[:k].copy_(U, non_blocking=True)
+        if U.is_cuda:
+            U_host[:U.shape[0]].copy_(U, non_blocking=True)
 
     e2e_s_ms = timed(e2e_seeded_step, args.steps, args.warmup)
     if not torch.equal(x0_seeded, x0_dev):
