@@ -49,6 +49,10 @@ __device__ unsigned long long g_ctc_tl[12][4];
   } while (0)
 #endif
 
+#ifndef CACTO_CTC_V8
+#define CACTO_CTC_V8 1
+#endif
+
 namespace ctc {
 
 constexpr int HP = 64;
@@ -146,6 +150,21 @@ CACTO_D void d1h(float z, float& d1, float& h) {
   }
 }
 
+// 32-byte aligned destinations (the [g ; zbar] factor rows, 256 B apart): two 256-bit
+// stores (STG.E.ENL2.256) instead of four 128-bit ones
+CACTO_D void st16g_v8(float* dst, const float (&v)[16]) {
+#if CACTO_CTC_V8
+#pragma unroll
+  for (int q = 0; q < 16; q += 8)
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + q), "f"(v[q]),
+                 "f"(v[q + 1]), "f"(v[q + 2]), "f"(v[q + 3]), "f"(v[q + 4]), "f"(v[q + 5]), "f"(v[q + 6]),
+                 "f"(v[q + 7])
+                 : "memory");
+#else
+#pragma unroll
+  for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+#endif
+}
 CACTO_D void st16g(float* dst, const float (&v)[16]) {
 #pragma unroll
   for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
@@ -486,7 +505,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         st16(TG + 128 + c0, g);
         put_ab(g);
         handoff();  // S2: s_2 = g_2 W_2
-        if (valid) st16g(a.GZ[2] + gb * 64 + c0, g);
+        if (valid) st16g_v8(a.GZ[2] + gb * 64 + c0, g);
       }
       for (int l = 1; l >= 0; --l) {  // g_l = act'(z_l) s_{l+1}
         wait_done();
@@ -501,7 +520,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         st16(TG + 64 * l + c0, g);
         put_ab(g);
         handoff();  // S1: s_1 = g_1 W_1 ; S0: s_0 = g_0 W_0 (N = 16)
-        if (valid) st16g(a.GZ[l] + gb * 64 + c0, g);
+        if (valid) st16g_v8(a.GZ[l] + gb * 64 + c0, g);
       }
       // errors, loss, u_0 (nets.py:268-277)
       wait_done();
@@ -584,7 +603,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       }
       put_ab(zb);
       handoff();  // B2: abar_2 = zbar_2 W_2
-      if (valid) st16g(a.GZ[2] + (B + gb) * 64 + c0, zb);
+      if (valid) st16g_v8(a.GZ[2] + (B + gb) * 64 + c0, zb);
       for (int l = 1; l >= 0; --l) {
         wait_done();
         float ab[16], z[16], zeta[16];
@@ -599,7 +618,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           put_ab(zb);
           handoff();  // B1: abar_1 = zbar_1 W_1
         }
-        if (valid) st16g(a.GZ[l] + (B + gb) * 64 + c0, zb);
+        if (valid) st16g_v8(a.GZ[l] + (B + gb) * 64 + c0, zb);
       }
     }
     // loss partial of this CTA
