@@ -53,6 +53,10 @@ __device__ unsigned long long g_ctc_tl[12][4];
 #define CACTO_CTC_V8 1
 #endif
 
+#ifndef CACTO_CTC_SCATTER_COALESCED
+#define CACTO_CTC_SCATTER_COALESCED 1
+#endif
+
 namespace ctc {
 
 constexpr int HP = 64;
@@ -782,6 +786,52 @@ __global__ void reduce_scatter_grads_kernel(const PartSet ps, int cols0, float* 
   if (lane == 0) slot[dst] += s;
 }
 
+// the same reduction with coalesced reads: layers 0..2 one THREAD per gradient entry,
+// consecutive threads on consecutive (row, column) entries of the [rows][ncol] partials,
+// each summing its entry's split partials in split order (a fixed order: deterministic;
+// the warp-per-entry form read one 32-byte sector per partial and lane); the output
+// row (65 entries over ~4 x SMs partials) keeps one warp per entry
+__global__ void reduce_scatter_coalesced_kernel(const PartSet ps, int cols0, float* slot, int64_t w0, int64_t b0,
+                                                int64_t w1, int64_t b1, int64_t w2, int64_t b2, int64_t w3,
+                                                int64_t b3, int n_thr) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n_thr) {
+    int l, nc;
+    if (e < HP * 17) {
+      l = 0, nc = 17;
+    } else if ((e -= HP * 17) < HP * 65) {
+      l = 1, nc = 65;
+    } else {
+      e -= HP * 65, l = 2, nc = 65;
+    }
+    const int o = e / nc, c = e - o * nc;
+    int64_t dst;
+    if (l == 0) {
+      if (c == 16) dst = b0 + o;
+      else if (c < cols0) dst = w0 + (int64_t)o * cols0 + c;
+      else return;
+    } else {
+      dst = (c == 64 ? (l == 1 ? b1 : b2) + o : (l == 1 ? w1 : w2) + (int64_t)o * HP + c);
+    }
+    const float* p = ps.p[l] + e;
+    const int64_t st = ps.stride[l];
+    float s0 = 0.f, s1 = 0.f;  // even / odd splits, then one add: a fixed order
+    int z = 0;
+    for (; z + 1 < ps.splits[l]; z += 2) {
+      s0 += p[z * st];
+      s1 += p[(z + 1) * st];
+    }
+    if (z < ps.splits[l]) s0 += p[z * st];
+    slot[dst] += s0 + s1;
+    return;
+  }
+  // output row: warp per entry over the out_row partials
+  const int we = (e - n_thr) >> 5, lane = threadIdx.x & 31;
+  if (we > HP) return;
+  const float sum = split_sum(ps, 3, we, lane);
+  if (lane == 0) slot[we < HP ? w3 + we : b3] += sum;
+}
+
 // ---- weight gradients of layers 0..2 on the tensor cores, fp16 pairs -----------------
 // gW_l[o][c] = alpha * sum_b G_l[b][o] * U_l[b][c] over the 2B rows b (g then zbar in G,
 // u then a | bias column in U): the per-sample factors critic_tc_kernel streamed as fp32
@@ -1272,9 +1322,17 @@ int critic_tc_loss(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cacto_bat
     }
   }
   if (aux) cudaStreamWaitEvent(st, aux->join, 0);
-  const int items = ctc::scatter_items(lo.cols[0]);
-  ctc::reduce_scatter_grads_kernel<<<(items * 32 + 255) / 256, 256, 0, st>>>(
-      ps, lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1], lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);
+  if (CACTO_CTC_SCATTER_COALESCED && wgrad_enabled()) {
+    const int n_thr = ctc::HP * 17 + 2 * ctc::HP * 65;  // the wgrad partials' [rows][ncol] entries
+    const int total = (n_thr + 31) / 32 * 32 + (ctc::HP + 1) * 32;
+    ctc::reduce_scatter_coalesced_kernel<<<(total + 255) / 256, 256, 0, st>>>(
+        ps, lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1], lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3],
+        (n_thr + 31) / 32 * 32);
+  } else {
+    const int items = ctc::scatter_items(lo.cols[0]);
+    ctc::reduce_scatter_grads_kernel<<<(items * 32 + 255) / 256, 256, 0, st>>>(
+        ps, lo.cols[0], slot, lo.w[0], lo.b[0], lo.w[1], lo.b[1], lo.w[2], lo.b[2], lo.w[3], lo.b[3]);
+  }
   return check_launch("critic_tc reductions");
 }
 
