@@ -156,6 +156,57 @@ CACTO_D void d1h(float z, float& d1, float& h) {
 
 // 32-byte aligned destinations (the [g ; zbar] factor rows, 256 B apart): two 256-bit
 // stores (STG.E.ENL2.256) instead of four 128-bit ones
+using rtc::f2add;
+using rtc::f2mul;
+using rtc::f2pack;
+using rtc::f2sub;
+using rtc::f2unpack;
+
+// the activation of 16 scaled accumulators D = S z (ELU: packed fp32x2, tcmlp.cuh elu2)
+template <int ACT>
+CACTO_D void act16(float (&v)[16]) {
+  if constexpr (ACT == CACTO_ACT_ELU) {
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) f2unpack(elu2(v[c], v[c + 1], ActTC<ACT>::S), v[c], v[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = ActTC<ACT>::apply(v[c]);
+  }
+}
+// act'(z) of 16 scaled pre-activations zs = S z.  ELU: S = 8 log2 e, so
+// act' = e^min(z,0) = ex2(min(zs,0) / 8) -- 1 exactly for zs >= 0, no select -- with
+// 2 min(zs,0) = zs - |zs| on packed FADD2 (one FMUL2 applies the 1/16)
+template <int ACT>
+CACTO_D void d1_16(const float (&zs)[16], float (&d1)[16]) {
+  if constexpr (ACT == CACTO_ACT_ELU) {
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) {
+      const uint64_t z2 = f2pack(zs[c], zs[c + 1]), az = f2pack(fabsf(zs[c]), fabsf(zs[c + 1]));
+      float m0, m1;
+      f2unpack(f2mul(f2sub(z2, az), f2pack(1.f / 16.f, 1.f / 16.f)), m0, m1);
+      d1[c] = tc::ex2_ftz(m0);
+      d1[c + 1] = tc::ex2_ftz(m1);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      float h;
+      d1h<ACT>(zs[c] * (1.f / ActTC<ACT>::S), d1[c], h);
+    }
+  }
+}
+// act''(z) / act'(z) of one scaled pre-activation (ELU: 0 for z > 0, else 1)
+template <int ACT>
+CACTO_D float h_of(float zs) {
+  if constexpr (ACT == CACTO_ACT_ELU) {
+    return zs > 0.f ? 0.f : 1.f;
+  } else {
+    float d1, h;
+    d1h<ACT>(zs * (1.f / ActTC<ACT>::S), d1, h);
+    return h;
+  }
+}
+
 CACTO_D void st16g_v8(float* dst, const float (&v)[16]) {
 #if CACTO_CTC_V8
 #pragma unroll
@@ -347,7 +398,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
     auto put_ab = [&](const float (&v)[16]) {  // backward operand, scaled by SB
       float w[16];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) w[c] = v[c] * SB;
+      for (int c = 0; c < 16; c += 2) f2unpack(f2mul(f2pack(v[c], v[c + 1]), f2pack(SB, SB)), w[c], w[c + 1]);
       put_a(w);
     };
     auto preload_bias = [&](uint32_t col, uint32_t bias_s, int layer) {
@@ -452,8 +503,7 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
           wait_done_t();
           float z[16];
           ld16(TT_D + c0, z);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) z[c] = AF::apply(z[c]);
+          act16<ACT>(z);
           put_at(z);
           if (l < 2) preload_bias(TT_D, bias_t, l + 1);
           else preload_out_bias(bias_t, TT_D);
@@ -462,9 +512,8 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         wait_done();
         float z[16];
         ld16(TZ + 64 * l + c0, z);
-        float av[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) av[c] = AF::apply(z[c]);
+        float(&av)[16] = z;
+        act16<ACT>(av);
         put_a(av);
         if (l < 2) preload_bias(TZ + 64 * (l + 1), bias_c, l + 1);
         else preload_out_bias(bias_c);
@@ -500,12 +549,10 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
       {
         float z[16], g[16];
         ld16(TZ + 128 + c0, z);
+        float d1[16];
+        d1_16<ACT>(z, d1);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float d1, h;
-          d1h<ACT>(z[c] * (1.f / S), d1, h);
-          g[c] = d1 * w3[c0 + c];
-        }
+        for (int c = 0; c < 16; ++c) g[c] = d1[c] * w3[c0 + c];
         st16(TG + 128 + c0, g);
         put_ab(g);
         handoff();  // S2: s_2 = g_2 W_2
@@ -515,11 +562,12 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         wait_done();
         float s[16], z[16], g[16];
         tc::tmem_ld16x2_wait(lrow + TD + c0, lrow + TZ + 64 * l + c0, s, z);
+        float d1[16];
+        d1_16<ACT>(z, d1);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float d1, h;
-          d1h<ACT>(z[c] * (1.f / S), d1, h);
-          g[c] = d1 * s[c] * RS;
+        for (int c = 0; c < 16; c += 2) {
+          const uint64_t gp = f2mul(f2mul(f2pack(d1[c], d1[c + 1]), f2pack(s[c], s[c + 1])), f2pack(RS, RS));
+          f2unpack(gp, g[c], g[c + 1]);
         }
         st16(TG + 64 * l + c0, g);
         put_ab(g);
@@ -559,13 +607,13 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         wait_done();
         float rv[16], z[16], g[16], u[16];
         tc::tmem_ld16x3_wait(lrow + TD + c0, lrow + TZ + 64 * l + c0, lrow + TG + 64 * l + c0, rv, z, g);
+        float d1[16];
+        d1_16<ACT>(z, d1);
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-          float d1, h;
-          d1h<ACT>(z[c] * (1.f / S), d1, h);
           const float rr_ = rv[c] * RS;
-          g[c] = h * g[c] * rr_;  // zeta_l
-          u[c] = d1 * rr_;
+          g[c] = h_of<ACT>(z[c]) * g[c] * rr_;  // zeta_l
+          u[c] = d1[c] * rr_;
         }
         st16(TG + 64 * l + c0, g);
         if (l < 2) {
@@ -595,12 +643,10 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         const float dlt = del_sh[r];
         float z[16], zeta[16];
         tc::tmem_ld16x2_wait(lrow + TZ + 128 + c0, lrow + TG + 128 + c0, z, zeta);
+        float d1[16];
+        d1_16<ACT>(z, d1);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float d1, h;
-          d1h<ACT>(z[c] * (1.f / S), d1, h);
-          zb[c] = d1 * (dlt * w3[c0 + c]) + zeta[c];
-        }
+        for (int c = 0; c < 16; ++c) zb[c] = d1[c] * (dlt * w3[c0 + c]) + zeta[c];
         // no second barrier before the next tile rewrites del_sh: that happens >= 10
         // layer hand-offs later, each needing all 16 epilogue warps (full_bar), so
         // every read above is done by then
@@ -612,12 +658,10 @@ __global__ void __launch_bounds__(ctc::NTHR, 1) critic_tc_kernel(const ctc::Args
         wait_done();
         float ab[16], z[16], zeta[16];
         tc::tmem_ld16x3_wait(lrow + TD + c0, lrow + TZ + 64 * l + c0, lrow + TG + 64 * l + c0, ab, z, zeta);
+        float d1[16];
+        d1_16<ACT>(z, d1);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float d1, h;
-          d1h<ACT>(z[c] * (1.f / S), d1, h);
-          zb[c] = d1 * ab[c] * RS + zeta[c];
-        }
+        for (int c = 0; c < 16; ++c) zb[c] = d1[c] * ab[c] * RS + zeta[c];
         if (l == 1) {
           put_ab(zb);
           handoff();  // B1: abar_1 = zbar_1 W_1
