@@ -163,7 +163,11 @@ int cacto_rollout(const cacto_system_t* sys, const cacto_cost_t* cost, const cac
  * (coalesced per step), so one cost rollout can also keep every candidate's
  * controls and the kept warm starts are a column take (cacto_take_columns)
  * instead of a second rollout (trainer.py:192-193 re-rolls the same starts). */
-enum { CACTO_ROLLOUT_U_TIME_MAJOR = 1 };
+enum { CACTO_ROLLOUT_U_TIME_MAJOR = 1,
+       /* U as [t_hor, N, m]: a step's controls of a start contiguous (coalesced per
+        * step too); the kept warm starts are then a step take (cacto_take_steps) that
+        * reads one 32-byte sector per kept start and step */
+       CACTO_ROLLOUT_U_STEP_MAJOR = 2 };
 int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
                      const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
                      int32_t flags, void* U, void* X, void* step_costs, void* cost_to_go, void* stream);
@@ -180,6 +184,10 @@ int cacto_rollout_score(const cacto_system_t* sys, const cacto_cost_t* cost, con
 /* dst[i, r] = src[r, idx[i]] for r < R, i < K: src [R, N] (dtype), dst [K, R] */
 int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int64_t N, const int64_t* idx, int64_t K,
                        void* dst, void* stream);
+/* dst [K, T, M] (dtype) <- rows idx[k] of a step-major src [T, N, M]: the kept
+ * warm starts out of a CACTO_ROLLOUT_U_STEP_MAJOR cost rollout (trainer.py:192-193). */
+int cacto_take_steps(int32_t dtype, const void* src, int64_t T, int64_t N, int32_t M, const int64_t* idx, int64_t K,
+                     void* dst, void* stream);
 /* dst[i, :] = src[idx[i], :], rows of R elements (dtype): the kept warm starts of a
  * start-major [N, T, m] U (trainer.py:192-193), one coalesced row copy each */
 int cacto_take_rows(int32_t dtype, const void* src, int64_t R, const int64_t* idx, int64_t K, void* dst,

@@ -80,6 +80,7 @@ _PBATCH = ctypes.POINTER(CactoBatch)
 _PI32 = ctypes.POINTER(ctypes.c_int32)
 
 ROLLOUT_U_TIME_MAJOR = 1   # CACTO_ROLLOUT_U_TIME_MAJOR
+ROLLOUT_U_STEP_MAJOR = 2   # CACTO_ROLLOUT_U_STEP_MAJOR
 FULL_HORIZON = -1          # CACTO_FULL_HORIZON
 
 # symbol -> (restype, argtypes); mirrors include/cacto_b200.h one to one
@@ -95,6 +96,7 @@ SIGNATURES = {
                                          _P]),
     "cacto_take_columns": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64, _P, _P]),
     "cacto_take_rows": (ctypes.c_int, [_I32, _P, _I64, _P, _I64, _P, _P]),
+    "cacto_take_steps": (ctypes.c_int, [_I32, _P, _I64, _I64, _I32, _P, _I64, _P, _P]),
     "cacto_rollout_score": (ctypes.c_int, [_PSYS, _PCOST, _PMLP, _I32, _PMLP, _PMLP, _P, _I32, _I64, _I32, _I32,
                                             _P, _P, _P, _P]),
     "cacto_score": (ctypes.c_int, [_I32, _PMLP, _PMLP, _P, _P, _I64, _P, _P]),

@@ -243,7 +243,40 @@ __global__ void take_rows_kernel(const T* __restrict__ src, int64_t R, const int
     }
   }
 }
+// dst[k, t, :] = src[t, idx[k], :] for a step-major U [T][N][M]: one warp per kept
+// start, lanes over its T steps (M contiguous values each: one sector per step instead
+// of one per (step, control) of the time-major column take), coalesced stores along
+// the kept start's [T][M] row
+template <typename T_>
+__global__ void take_steps_kernel(const T_* __restrict__ src, int64_t T, int64_t N, int M,
+                                  const int64_t* __restrict__ idx, int64_t K, T_* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < K; i += nw) {
+    const int64_t col = idx[i];
+    T_* d = dst + i * T * M;
+    for (int64_t t = lane; t < T; t += 32) {
+      const T_* s = src + (t * N + col) * M;
+      for (int j = 0; j < M; ++j) d[t * M + j] = __ldg(s + j);
+    }
+  }
+}
 }  // namespace cacto
+
+extern "C" int cacto_take_steps(int32_t dtype, const void* src, int64_t T, int64_t N, int32_t M, const int64_t* idx,
+                                int64_t K, void* dst, void* stream) {
+  if (T < 0 || N < 0 || M <= 0 || K < 0 || (T * K > 0 && (!src || !idx || !dst)))
+    return set_error(CACTO_EVALUE, "take_steps: bad arguments");
+  if (T * K == 0) return CACTO_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((K + 7) / 8, 32 * (int64_t)num_sms());
+  if (dtype == CACTO_F32)
+    take_steps_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)src, T, N, M, idx, K, (float*)dst);
+  else
+    take_steps_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)src, T, N, M, idx, K,
+                                                                       (double*)dst);
+  return check_launch("take_steps_kernel");
+}
 
 extern "C" int cacto_take_rows(int32_t dtype, const void* src, int64_t R, const int64_t* idx, int64_t K, void* dst,
                                void* stream) {
@@ -275,7 +308,9 @@ extern "C" int cacto_take_columns(int32_t dtype, const void* src, int64_t R, int
 extern "C" int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* cost, const cacto_mlp_t* actor,
                                 const double* x0, const int32_t* t0, int32_t t0_scalar, int64_t N, int32_t t_hor,
                                 int32_t flags, void* U, void* X, void* step_costs, void* cost_to_go, void* stream) {
-  if (flags & ~CACTO_ROLLOUT_U_TIME_MAJOR) return set_error(CACTO_EVALUE, "rollout: unknown flags %d", flags);
+  if ((flags & ~(CACTO_ROLLOUT_U_TIME_MAJOR | CACTO_ROLLOUT_U_STEP_MAJOR)) ||
+      (flags & CACTO_ROLLOUT_U_TIME_MAJOR && flags & CACTO_ROLLOUT_U_STEP_MAJOR))
+    return set_error(CACTO_EVALUE, "rollout: unknown flags %d", flags);
   if (!sys || !actor || !x0) return set_error(CACTO_EVALUE, "rollout: null argument");
   if (!system_dims_ok(sys)) return set_error(CACTO_EUNSUPPORTED, "rollout: unknown system kind %d / dims", sys->kind);
   if (N < 0) return set_error(CACTO_EVALUE, "rollout: N < 0");
@@ -298,7 +333,7 @@ extern "C" int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* c
     a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
     a.params = (const float*)actor->params;
     a.x0 = x0; a.t0 = t0; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor; a.t_stride = stride;
-    a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : 0;
+    a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : ((flags & CACTO_ROLLOUT_U_STEP_MAJOR) ? 2 : 0);
     a.U = (float*)U; a.X = (float*)X; a.SC = (float*)step_costs; a.C = (float*)cost_to_go;
     return dispatch_rollout(a, sys->kind, sh.hp, st);
   }
@@ -310,7 +345,7 @@ extern "C" int cacto_rollout_ex(const cacto_system_t* sys, const cacto_cost_t* c
   a.nh = sh.nh; a.out = sh.out; a.act = sh.act; a.head = sh.head;
   a.params = (const double*)actor->params;
   a.x0 = x0; a.t0 = t0; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor; a.t_stride = stride;
-  a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : 0;
+  a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : ((flags & CACTO_ROLLOUT_U_STEP_MAJOR) ? 2 : 0);
   a.U = (double*)U; a.X = (double*)X; a.SC = (double*)step_costs; a.C = (double*)cost_to_go;
   return dispatch_rollout(a, sys->kind, sh.hp, st);
 }
@@ -329,7 +364,9 @@ extern "C" int cacto_rollout_score(const cacto_system_t* sys, const cacto_cost_t
                                    void* U, void* cost_to_go, void* scores, void* stream) {
   if (mode < 0 || mode > 2) return set_error(CACTO_EVALUE, "rollout_score: unknown mode %d", mode);
   if (!scores) return set_error(CACTO_EVALUE, "rollout_score: null scores");
-  if (flags & ~CACTO_ROLLOUT_U_TIME_MAJOR) return set_error(CACTO_EVALUE, "rollout_score: unknown flags %d", flags);
+  if ((flags & ~(CACTO_ROLLOUT_U_TIME_MAJOR | CACTO_ROLLOUT_U_STEP_MAJOR)) ||
+      (flags & CACTO_ROLLOUT_U_TIME_MAJOR && flags & CACTO_ROLLOUT_U_STEP_MAJOR))
+    return set_error(CACTO_EVALUE, "rollout_score: unknown flags %d", flags);
   if (!sys || !actor || !x0) return set_error(CACTO_EVALUE, "rollout_score: null argument");
   if (!system_dims_ok(sys)) return set_error(CACTO_EUNSUPPORTED, "rollout_score: unknown system kind %d", sys->kind);
   const bool need_std = mode != CACTO_SCORE_GAP, need_crit = mode != CACTO_SCORE_STD;
@@ -362,7 +399,7 @@ extern "C" int cacto_rollout_score(const cacto_system_t* sys, const cacto_cost_t
   a.params = (const float*)actor->params;
   a.x0 = x0; a.t0 = nullptr; a.t0_scalar = t0_scalar; a.N = N; a.t_hor = t_hor;
   a.t_stride = t_hor;
-  a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : 0;
+  a.u_tmajor = (flags & CACTO_ROLLOUT_U_TIME_MAJOR) ? 1 : ((flags & CACTO_ROLLOUT_U_STEP_MAJOR) ? 2 : 0);
   a.U = (float*)U; a.C = (float*)cost_to_go;
   if (need_std) {
     a.pre_kind[a.n_pre] = 0;

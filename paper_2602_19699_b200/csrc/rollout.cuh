@@ -21,8 +21,10 @@ struct RolloutArgs {
   int64_t N;
   int t_hor;      // >= 0 fixed horizon; CACTO_FULL_HORIZON (-1) -> per-start t_max - t0
   int t_stride;   // row stride of the per-step outputs
-  int u_tmajor;   // U as [t_hor][m][N] (CACTO_ROLLOUT_U_TIME_MAJOR)
+  int u_tmajor;   // U layout: 0 [N][t_stride][m], 1 [t_hor][m][N] (CACTO_ROLLOUT_U_TIME_MAJOR),
+                  // 2 [t_hor][N][m] (CACTO_ROLLOUT_U_STEP_MAJOR)
   CACTO_D int64_t u_at(int64_t gi, int k, int j, int m) const {
+    if (u_tmajor == 2) return ((int64_t)k * N + gi) * m + j;
     return u_tmajor ? ((int64_t)k * m + j) * N + gi : (gi * t_stride + k) * m + j;
   }
   T* U;

@@ -27,8 +27,10 @@ import os
 # or start-major [N, T, m] (take = one coalesced row copy per kept start, but
 # K1's 12-byte strided writes cost more than the take saves: measured manipulator3
 # step 4.12 -> 4.19 ms, dubins 0.83 -> 0.90 ms, profiles/README.md).
-# CACTO_WARM_TMAJOR=0 selects start-major (A/B only).
-_TMAJOR = os.environ.get("CACTO_WARM_TMAJOR", "1") == "1"
+# Layout of every candidate's controls in the cost rollout (CACTO_WARM_LAYOUT):
+# "step" [T, N, m] (kept warm starts = a step take), "time" [T, m, N] (a column take),
+# "start" [N, T, m] (a row take; A/B only).
+_LAYOUT = os.environ.get("CACTO_WARM_LAYOUT", "step")
 # host warm-start output: the take kernel writes the pinned host buffer directly
 # (zero-copy, "1") or runs in chunks whose device-to-host copies on a side stream
 # overlap the next chunk's take ("0", default; measured faster)
@@ -153,11 +155,27 @@ class BicPipeline:
 
     def _u_all(self, N, T, dt, dev):
         """(pointer, flags) of the buffer the cost rollout writes every candidate's
-        controls into (start-major [N, T, m], or time-major under _TMAJOR)."""
-        shape = (T, self.model.m, N) if _TMAJOR else (N, T, self.model.m)
+        controls into (step-major [T, N, m], time-major [T, m, N] or start-major [N, T, m],
+        _LAYOUT)."""
+        m = self.model.m
+        shape = {"step": (T, N, m), "time": (T, m, N)}.get(_LAYOUT, (N, T, m))
         if getattr(self, "u_all", None) is None or tuple(self.u_all.shape) != shape or self.u_all.dtype != dt:
             self.u_all = torch.empty(shape, device=dev, dtype=dt)
-        return self.u_all.data_ptr(), (_lib.ROLLOUT_U_TIME_MAJOR if _TMAJOR else 0)
+        flags = {"step": _lib.ROLLOUT_U_STEP_MAJOR, "time": _lib.ROLLOUT_U_TIME_MAJOR}.get(_LAYOUT, 0)
+        return self.u_all.data_ptr(), flags
+
+    def _take(self, sel_ptr: int, K: int, dst_ptr: int, N: int, T: int, stream):
+        """The kept starts' controls out of self.u_all into dst [K, T, m] (one launch)."""
+        m = self.model.m
+        if _LAYOUT == "step":
+            _lib.call("cacto_take_steps", abi_dtype(self.precision), self.u_all.data_ptr(), T, N, m, sel_ptr, K,
+                      dst_ptr, stream)
+        elif _LAYOUT == "time":
+            _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), T * m, N, sel_ptr, K,
+                      dst_ptr, stream)
+        else:
+            _lib.call("cacto_take_rows", abi_dtype(self.precision), self.u_all.data_ptr(), T * m, sel_ptr, K,
+                      dst_ptr, stream)
 
     def rollout_costs(self, x0: torch.Tensor, t0: int = 0, keep_controls: bool = False) -> torch.Tensor:
         """K1 cost-to-go of every candidate; with keep_controls the same launch
@@ -231,7 +249,7 @@ class BicPipeline:
             U = torch.empty((K, T, self.model.m), device=_dev(x0), dtype=dt)
         if K == 0:
             return (out[:0] if out is not None else U), 0
-        if reuse and out is not None and not _WARM_ZC and _TMAJOR and not out.is_cuda:
+        if reuse and out is not None and not _WARM_ZC and not out.is_cuda:
             # chunked take; chunk c's copy to the pinned host buffer (side stream, copy
             # engine) overlaps chunk c + 1's take; the caller's stream waits for the
             # last copy, so the returned host rows are complete in stream order
@@ -247,9 +265,8 @@ class BicPipeline:
                 c0, c1 = bounds[c], bounds[c + 1]
                 if c1 == c0:
                     continue
-                _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), row, N,
-                          sel.data_ptr() + c0 * sel.element_size(), c1 - c0, U.data_ptr() + c0 * row * es,
-                          main.cuda_stream)
+                self._take(sel.data_ptr() + c0 * sel.element_size(), c1 - c0, U.data_ptr() + c0 * row * es, N, T,
+                           main.cuda_stream)
                 ev = torch.cuda.Event()
                 ev.record(main)
                 cs.wait_event(ev)
@@ -263,12 +280,7 @@ class BicPipeline:
         if reuse:
             # the kept starts' controls from the cost rollout (same actor, start and t0:
             # the trajectories trainer.py:192-193 would roll out again)
-            if _TMAJOR:
-                _lib.call("cacto_take_columns", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
-                          N, sel.data_ptr(), K, U.data_ptr(), _stream())
-            else:
-                _lib.call("cacto_take_rows", abi_dtype(self.precision), self.u_all.data_ptr(), T * self.model.m,
-                          sel.data_ptr(), K, U.data_ptr(), _stream())
+            self._take(sel.data_ptr(), K, U.data_ptr(), N, T, _stream())
             if out is not None and U.is_cuda and not out.is_cuda:
                 out[:K].copy_(U, non_blocking=True)
                 U = out[:K]

@@ -607,3 +607,19 @@ def test_take_columns_bitwise(dtype, R, N, K):
     _lib.call("cacto_take_columns", _lib.F32 if dtype == "f32" else _lib.F64, src.data_ptr(), R, N, idx.data_ptr(),
               K, dst.data_ptr(), torch.cuda.current_stream().cuda_stream)
     assert torch.equal(dst, src[:, idx].T)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("T,N,M,K", [(100, 65536, 3, 6553), (7, 100, 2, 33), (33, 5000, 6, 5000), (1, 3, 1, 1)])
+def test_take_steps_bitwise(dtype, T, N, M, K):
+    """cacto_take_steps (kept warm starts out of K1's step-major U [T, N, m]):
+    dst[k, t, :] = src[t, idx[k], :]."""
+    from paper_2602_19699_b200 import _lib
+    dt = torch.float32 if dtype == "f32" else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(T * 7 + K)
+    src = torch.randn((T, N, M), device="cuda", dtype=dt, generator=g)
+    idx = torch.randint(0, N, (K,), device="cuda", generator=g)
+    dst = torch.empty((K, T, M), device="cuda", dtype=dt)
+    _lib.call("cacto_take_steps", _lib.F32 if dtype == "f32" else _lib.F64, src.data_ptr(), T, N, M, idx.data_ptr(),
+              K, dst.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert torch.equal(dst, src[:, idx, :].transpose(0, 1))
