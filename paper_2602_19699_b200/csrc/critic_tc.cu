@@ -920,7 +920,11 @@ struct __align__(64) WgradArgs {
 CACTO_D void split8(const float (&v)[8], uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) rtc::split2(v[2 * j] * WG_SB, v[2 * j + 1] * WG_SB, h[j], l[j]);
+  for (int j = 0; j < 4; ++j) {
+    float a0, a1;  // the SB scaling on packed FMUL2
+    rtc::f2unpack(rtc::f2mul(rtc::f2pack(v[2 * j], v[2 * j + 1]), rtc::f2pack(WG_SB, WG_SB)), a0, a1);
+    rtc::split2(a0, a1, h[j], l[j]);
+  }
   hi = make_uint4(h[0], h[1], h[2], h[3]);
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
