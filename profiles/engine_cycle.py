@@ -14,7 +14,7 @@ from paper_2602_19699_b200.device import set_precision  # noqa: E402
 from paper_2602_19699_b200.engine import UpdateEngine  # noqa: E402
 
 
-def main(M=1000, B=128):
+def build_engine(B=128):
     set_precision("fp32")
     spec, fld = specs.config("pointmass")
     rng = np.random.default_rng(0)
@@ -29,7 +29,11 @@ def main(M=1000, B=128):
     buf = B_buffer.ReplayBuffer(spec.n, spec.m, spec.t_max, capacity=1 << 20)
     buf.push_many(B_buffer.SampleBatch(xa, rng.normal(size=(R, spec.m)), rng.normal(size=R), rng.normal(size=(R, spec.n)),
                                        xk, spec.t_max))
-    eng = UpdateEngine(spec, fld, actor, critic, target, std, buf, minibatch=B)
+    return UpdateEngine(spec, fld, actor, critic, target, std, buf, minibatch=B)
+
+
+def main(M=1000, B=128):
+    eng = build_engine(B)
     eng.run(M, np.random.default_rng(1))
     torch.cuda.synchronize()
     for rep in range(3):
