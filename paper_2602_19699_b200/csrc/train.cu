@@ -17,6 +17,10 @@
 #include "net.cuh"
 #include "systems.cuh"
 
+#ifndef CACTO_CRITIC_FUSED_TARGET
+#define CACTO_CRITIC_FUSED_TARGET 1  // bootstrap target forward inside critic_kernel
+#endif
+
 namespace cacto {
 
 template <typename T>
@@ -168,6 +172,8 @@ struct CriticArgs {
   T inv_denom;
   T k_s;
   const T* v_next;  // [rows] target value at x_{+k} (bootstrap) or null
+  const T* tparams; // target net (the critic's shape) evaluated in-kernel at x_{+k}, or null
+  NetConst<T> nc_t; // its input normalisation
   T* ws;            // [grid][P+1]
   int smem_slot;    // accumulate the CTA's gradient slot in shared memory, store it once
 };
@@ -196,6 +202,16 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
   p += S;
   T* EG = p;  // [n][S] gradient errors
   p += (size_t)CACTO_MAX_IN * S;
+  // bootstrap target forward in the same kernel (the critic's shape, its own staged
+  // copy): one launch per critic update instead of rows_forward_kernel + critic_kernel
+  NetSmem<T, HP, IP, TL::KS> tnet;
+  T* VT = nullptr;  // [S] target values of the tile
+  if (a.tparams) {
+    p = tnet.carve(p, a.nh, a.in, 1);
+    VT = p;
+    p += S;
+    tnet.stage(a.tparams);
+  }
 
   net.stage(a.params);
   const int64_t P_total = a.off.total;
@@ -211,6 +227,16 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
   const int64_t ntiles = (a.b.rows + S - 1) / S;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t base = t * S;
+    if (a.tparams) {  // V_target(x_{+k}) of the tile (nets.py:247-251), as rows_forward_kernel
+      __syncthreads();
+      load_input_tile<TL>(A0, IP, a.in, a.nc_t,
+                            [&](int s) { return base + s < a.b.rows ? a.b.row(base + s) : (int64_t)-1; },
+                            [&](int64_t r, int c) { return a.b.xa_plus_k[r * a.in + c]; });
+      __syncthreads();
+      const T* lastt = forward_hidden(tl, tnet, a.act, A0, P, Q, (T*)nullptr);
+      forward_output<TL>(tnet, lastt, [&](int s, int, T o) { VT[s] = o; });
+      __syncthreads();
+    }
     load_input_tile<TL>(A0, IP, a.in, a.nc,
                           [&](int s) { return base + s < a.b.rows ? a.b.row(base + s) : (int64_t)-1; },
                           [&](int64_t r, int c) { return a.b.xa[r * a.in + c]; });
@@ -219,9 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1) critic_kernel(const CriticArgs<T>
       if (base + s < a.b.rows) {
         int64_t r = a.b.row(base + s);
         y = a.b.v_bar[r];
-        if (a.v_next) {  // nets.py:247-251
+        if (a.v_next || a.tparams) {  // nets.py:247-251
           bool gate = a.b.xa_plus_k[r * (n + 1) + n] < (T)a.b.t_max;
-          y = y + (gate ? a.v_next[base + s] : T(0));
+          y = y + (gate ? (a.tparams ? VT[s] : a.v_next[base + s]) : T(0));
         }
       }
       EV[s] = y;
@@ -663,6 +689,7 @@ template <typename T, int HP, int IP, int S>
 static int launch_critic_s(const CriticArgs<T>& a, int64_t rows, int* grid_out, cudaStream_t st) {
   size_t el = net_elems<T, HP, IP>(a.nh, 1) + 2 * (size_t)IP * S + (2 * (size_t)a.nh + 2) * HP * S + S +
               (size_t)CACTO_MAX_IN * S;
+  if (a.tparams) el += net_elems<T, HP, IP>(a.nh, 1) + S;  // the staged target net + its tile values
   size_t bytes = el * sizeof(T);
   auto kern = critic_kernel<T, HP, IP, S>;
   CriticArgs<T> b = a;
@@ -702,18 +729,37 @@ static int critic_entry(const cacto_mlp_t* c, const cacto_mlp_t* tgt, const cact
   a.k_s = (T)k_s;
   a.ws = (T*)ws;
   if (boot && tgt) {
-    T* vnext = (T*)scratch_of(c, ws);
-    int rc = cacto_forward_rows(tgt, b, /*xa_plus_k*/ 1, vnext, st);
-    if (rc) return rc;
-    a.v_next = vnext;
+    const NetShape tsh = shape_of(*tgt);
+    if (CACTO_CRITIC_FUSED_TARGET && tsh.hp == sh.hp && tsh.ip == sh.ip && tsh.nh == sh.nh && tsh.in == sh.in &&
+        tsh.act == sh.act && tsh.head == CACTO_HEAD_LINEAR && tgt->dtype == c->dtype) {
+      a.tparams = (const T*)tgt->params;
+      a.nc_t = net_const<T>(*tgt);
+    } else {
+      T* vnext = (T*)scratch_of(c, ws);
+      int rc = cacto_forward_rows(tgt, b, /*xa_plus_k*/ 1, vnext, st);
+      if (rc) return rc;
+      a.v_next = vnext;
+    }
   }
   int grid = 0;
-  int rc = CACTO_EUNSUPPORTED;
-  if (sh.hp == 32 && sh.ip == 8) rc = launch_critic<T, 32, 8>(a, b->rows, &grid, st);
-  else if (sh.hp == 32 && sh.ip == 16) rc = launch_critic<T, 32, 16>(a, b->rows, &grid, st);
-  else if (sh.hp == 64 && sh.ip == 8) rc = launch_critic<T, 64, 8>(a, b->rows, &grid, st);
-  else if (sh.hp == 64 && sh.ip == 16) rc = launch_critic<T, 64, 16>(a, b->rows, &grid, st);
-  else return set_error(CACTO_EUNSUPPORTED, "critic_loss: hidden %d / input %d not built", sh.hp, sh.in);
+  auto launch = [&]() {
+    if (sh.hp == 32 && sh.ip == 8) return launch_critic<T, 32, 8>(a, b->rows, &grid, st);
+    if (sh.hp == 32 && sh.ip == 16) return launch_critic<T, 32, 16>(a, b->rows, &grid, st);
+    if (sh.hp == 64 && sh.ip == 8) return launch_critic<T, 64, 8>(a, b->rows, &grid, st);
+    if (sh.hp == 64 && sh.ip == 16) return launch_critic<T, 64, 16>(a, b->rows, &grid, st);
+    return set_error(CACTO_EUNSUPPORTED, "critic_loss: hidden %d / input %d not built", sh.hp, sh.in);
+  };
+  int rc = launch();
+  if (rc == CACTO_EUNSUPPORTED && a.tparams) {
+    // the staged target does not fit beside the tile (fp64, wide tiles): the separate
+    // target forward, then the plain kernel (nothing was launched above)
+    a.tparams = nullptr;
+    T* vnext = (T*)scratch_of(c, ws);
+    rc = cacto_forward_rows(tgt, b, /*xa_plus_k*/ 1, vnext, st);
+    if (rc) return rc;
+    a.v_next = vnext;
+    rc = launch();
+  }
   *n_partials = grid;
   return rc;
 }
