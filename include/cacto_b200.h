@@ -339,6 +339,14 @@ int cacto_reduce_adam_graph(int32_t dtype, const void* workspace, int32_t n_part
                             void* m, void* v, const int64_t* counter, const int64_t* step_base, const double* bc1,
                             const double* bc2, double lr, double beta1, double beta2, double eps, void* target,
                             double tau, void* loss_base, void* stream);
+/* the same, also writing the updated parameters into slot (*counter % ring_n) of a
+ * [ring_n][ring_ld] buffer: the pipelined M-cycle loop's per-cycle critic copy
+ * (cacto_ring_copy save) fused into the update. */
+int cacto_reduce_adam_graph_ring(int32_t dtype, const void* workspace, int32_t n_partials, int64_t P, void* params,
+                                 void* m, void* v, const int64_t* counter, const int64_t* step_base, const double* bc1,
+                                 const double* bc2, double lr, double beta1, double beta2, double eps, void* target,
+                                 double tau, void* loss_base, void* ring, int64_t ring_n, int64_t ring_ld,
+                                 void* stream);
 /* ++(*counter) on device (closes one captured update cycle) */
 int cacto_counter_tick(int64_t* counter, void* stream);
 /* span[i] = *base + i (i < k), then *base += k: one launch gives the k cycles of a

@@ -125,6 +125,8 @@ SIGNATURES = {
                                          _P, _P, _P]),
     "cacto_reduce_adam_graph": (ctypes.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D,
                                                 _D, _P, _D, _P, _P]),
+    "cacto_reduce_adam_graph_ring": (ctypes.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D,
+                                                     _D, _P, _D, _P, _P, _I64, _I64, _P]),
     "cacto_counter_tick": (ctypes.c_int, [_P, _P]),
     "cacto_ring_copy": (ctypes.c_int, [_I32, _P, _P, _I64, _I64, _I64, _P, _I32, _P]),
     "cacto_counter_span": (ctypes.c_int, [_P, _P, _I32, _P]),

@@ -110,8 +110,12 @@ template <typename T>
 __global__ void reduce_adam_graph_kernel(const T* __restrict__ ws, int n, int64_t P, T* p, T* m, T* v,
                                          const int64_t* counter, const int64_t* step_base, const double* bc1,
                                          const double* bc2, T lr, T b1, T b2, T eps, T one_m_b1, T one_m_b2, T* tgt,
-                                         T one_m_tau, T tau, T* loss_base) {
+                                         T one_m_tau, T tau, T* loss_base, T* ring = nullptr, int64_t ring_n = 1,
+                                         int64_t ring_ld = 0) {
   const int64_t c = *counter;
+  // optional: the updated parameters also into ring slot c % ring_n (the ring_copy of
+  // the pipelined M-cycle loop, engine.py, fused into the update: one launch less)
+  T* rslot = ring ? ring + (c % ring_n) * ring_ld : nullptr;
   const int64_t t = *step_base + c + 1;
   AdamK<T> k;
   k.lr = lr;
@@ -134,6 +138,7 @@ __global__ void reduce_adam_graph_kernel(const T* __restrict__ ws, int n, int64_
     m[i] = mm;
     v[i] = vv;
     if (tgt) tgt[i] = r_add(r_mul(one_m_tau, tgt[i]), r_mul(tau, pp));
+    if (rslot) rslot[i] = pp;
   }
 }
 
@@ -237,6 +242,29 @@ extern "C" int cacto_reduce_adam_graph(int32_t dtype, const void* workspace, int
     reduce_adam_graph_kernel<double><<<grid_of(P + 1), 256, 0, st>>>(
         (const double*)workspace, n_partials, P, (double*)params, (double*)m, (double*)v, counter, step_base, bc1,
         bc2, lr, beta1, beta2, eps, 1.0 - beta1, 1.0 - beta2, (double*)target, 1.0 - tau, tau, (double*)loss_base);
+  return check_launch("reduce_adam_graph_kernel");
+}
+
+extern "C" int cacto_reduce_adam_graph_ring(int32_t dtype, const void* workspace, int32_t n_partials, int64_t P,
+                                            void* params, void* m, void* v, const int64_t* counter,
+                                            const int64_t* step_base, const double* bc1, const double* bc2, double lr,
+                                            double beta1, double beta2, double eps, void* target, double tau,
+                                            void* loss_base, void* ring, int64_t ring_n, int64_t ring_ld,
+                                            void* stream) {
+  if (!workspace || n_partials < 1 || P < 0 || !params || !m || !v || !counter || !step_base || !bc1 || !bc2 ||
+      !ring || ring_n < 1 || ring_ld < P)
+    return set_error(CACTO_EVALUE, "reduce_adam_graph_ring: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CACTO_F32)
+    reduce_adam_graph_kernel<float><<<grid_of(P + 1), 256, 0, st>>>(
+        (const float*)workspace, n_partials, P, (float*)params, (float*)m, (float*)v, counter, step_base, bc1, bc2,
+        (float)lr, (float)beta1, (float)beta2, (float)eps, (float)(1.0 - beta1), (float)(1.0 - beta2),
+        (float*)target, (float)(1.0 - tau), (float)tau, (float*)loss_base, (float*)ring, ring_n, ring_ld);
+  else
+    reduce_adam_graph_kernel<double><<<grid_of(P + 1), 256, 0, st>>>(
+        (const double*)workspace, n_partials, P, (double*)params, (double*)m, (double*)v, counter, step_base, bc1,
+        bc2, lr, beta1, beta2, eps, 1.0 - beta1, 1.0 - beta2, (double*)target, 1.0 - tau, tau, (double*)loss_base,
+        (double*)ring, ring_n, ring_ld);
   return check_launch("reduce_adam_graph_kernel");
 }
 

@@ -26,6 +26,7 @@ std, the dependency order of trainer.py:211-233.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Optional
 
 import numpy as np
@@ -113,6 +114,9 @@ class UpdateEngine:
         self._ensure_bc(max(int(max_steps), 1 + max(n.step for n in (self.actor, self.critic, self.std))))
         self.use_graphs = use_graphs
         self.K = 16          # cycles per captured chunk (pipelined schedule)
+        # ring of RC chunks of per-cycle critics: the critic chain may run RC - 1 chunks
+        # ahead of the actor chain (the std chain starts when the critic chain ends)
+        self.RC = int(os.environ.get("CACTO_RING_CHUNKS", "8"))
         self.cview = None
         self._graphs = None
         self._cap_M = 0
@@ -153,7 +157,7 @@ class UpdateEngine:
         d.denom = self.B if self.world > 1 else 0
         return d
 
-    def _adam(self, net: _Net, ws, npart, slot, target=None, loss=None, cptr=None):
+    def _adam(self, net: _Net, ws, npart, slot, target=None, loss=None, cptr=None, ring=None):
         bc1, bc2 = self.bc[(net.beta1, net.beta2)]
         if self.world > 1:
             # fold -> [grad | loss] -> sum over ranks -> replicated Adam (+ Polyak)
@@ -163,11 +167,14 @@ class UpdateEngine:
             parallel.allreduce_grads(g, self.dp_group)
             ws, npart = g, 1
         counter = self.cnt[slot:slot + 1].data_ptr() if cptr is None else cptr
-        _lib.call("cacto_reduce_adam_graph", net.dn.desc.dtype, ws.data_ptr(), npart, net.dn.count,
-                  net.dn.params.data_ptr(), net.m.data_ptr(), net.v.data_ptr(), counter,
-                  net.base.data_ptr(), bc1.data_ptr(), bc2.data_ptr(), net.lr, net.beta1, net.beta2, net.eps,
-                  None if target is None else target.params.data_ptr(), self.tau,
-                  None if loss is None else loss.data_ptr(), _stream())
+        args = (net.dn.desc.dtype, ws.data_ptr(), npart, net.dn.count, net.dn.params.data_ptr(), net.m.data_ptr(),
+                net.v.data_ptr(), counter, net.base.data_ptr(), bc1.data_ptr(), bc2.data_ptr(), net.lr, net.beta1,
+                net.beta2, net.eps, None if target is None else target.params.data_ptr(), self.tau,
+                None if loss is None else loss.data_ptr())
+        if ring is None:
+            _lib.call("cacto_reduce_adam_graph", *args, _stream())
+        else:  # the updated parameters also into ring slot (*counter % ring rows)
+            _lib.call("cacto_reduce_adam_graph_ring", *args, ring.data_ptr(), ring.shape[0], ring.shape[1], _stream())
 
     def _cycle_critic_actor(self):
         st = _stream()
@@ -206,10 +213,9 @@ class UpdateEngine:
         tgt = self.target if self.bootstrap else None
         _lib.call("cacto_critic_loss", self.critic.dn.desc, tgt.desc if tgt else None, bd, self.k_s,
                   int(self.bootstrap), self.ws_c.data_ptr(), self.ws_c.numel(), npart, st)
-        self._adam(self.critic, self.ws_c, npart.value, 0, target=self.target, loss=self.closs, cptr=c)
-        _lib.call("cacto_ring_copy", self.critic.dn.desc.dtype, self.cring.data_ptr(), c,
-                  self.cring.shape[0], self.cring.shape[1], self.critic.dn.count, self.critic.dn.params.data_ptr(),
-                  1, st)
+        # Adam + Polyak + this cycle's critic into the ring (ring_copy fused into the update)
+        self._adam(self.critic, self.ws_c, npart.value, 0, target=self.target, loss=self.closs, cptr=c,
+                   ring=self.cring)
         if cptr is None:
             _lib.call("cacto_counter_tick", c, st)
 
@@ -282,10 +288,10 @@ class UpdateEngine:
         if pipe and self.cview is None:
             self.cview = DeviceNet(self.critic.dn.to_mlp(), self.precision)
             ld = (self.critic.dn.count + 63) // 64 * 64   # 256/512-byte aligned ring slots
-            self.cring = torch.zeros((2 * self.K, ld), device=dev, dtype=torch_dtype(self.precision))
+            self.cring = torch.zeros((self.RC * self.K, ld), device=dev, dtype=torch_dtype(self.precision))
             # static descriptors of the ring slots (the actor chain's critic of cycle i)
             self.slot_desc = []
-            for r in range(2 * self.K):
+            for r in range(self.RC * self.K):
                 d = type(self.cview.desc).from_buffer_copy(self.cview.desc)
                 d.params = self.cring[r].data_ptr()
                 self.slot_desc.append(d)
@@ -325,8 +331,8 @@ class UpdateEngine:
         with torch.cuda.stream(side):
             if pipe:
                 graphs["c"] = chunk(self._cycle_critic, 0)
-                graphs["a0"] = chunk(self._cycle_actor, 2, self.slot_desc[:self.K])
-                graphs["a1"] = chunk(self._cycle_actor, 2, self.slot_desc[self.K:])
+                for q in range(self.RC):  # actor chunk j reads ring chunk j % RC
+                    graphs["a%d" % q] = chunk(self._cycle_actor, 2, self.slot_desc[q * self.K:(q + 1) * self.K])
                 graphs["s"] = chunk(self._cycle_std_err, 1)
             else:
                 for name, fn in (("ca", self._cycle_critic_actor), ("s", self._cycle_std)):
@@ -338,9 +344,9 @@ class UpdateEngine:
         self._graphs = graphs
 
     def _run_pipelined(self, M):
-        """critic chain | actor chain (one chunk of K cycles behind) | std chain (after
-        the last critic chunk), on three streams; the ring holds 2K cycles' critics, so
-        critic chunk j + 2 waits for actor chunk j.  A partial last chunk runs eager."""
+        """critic chain | actor chain (behind it) | std chain (after the last critic
+        chunk), on three streams; the ring holds RC chunks of K cycles' critics, so
+        critic chunk j + RC waits for actor chunk j.  A partial last chunk runs eager."""
         g = self._graphs
         K = self.K
         main = torch.cuda.current_stream()
@@ -355,8 +361,8 @@ class UpdateEngine:
         for j in range(nch):
             n = min(K, M - j * K)
             with torch.cuda.stream(sc):
-                if j >= 2:
-                    sc.wait_event(ev_a[j - 2])
+                if j >= self.RC:
+                    sc.wait_event(ev_a[j - self.RC])
                 if n == K:
                     g["c"].replay()
                 else:
@@ -366,7 +372,7 @@ class UpdateEngine:
             with torch.cuda.stream(sa):
                 sa.wait_event(ev_c[j])
                 if n == K:
-                    g["a0" if j % 2 == 0 else "a1"].replay()
+                    g["a%d" % (j % self.RC)].replay()
                 else:
                     for _ in range(n):
                         self._cycle_actor()
